@@ -1,0 +1,383 @@
+"""Benchmark: block-wise two-source extraction on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+A step is one pass of the hot path over one batch of synthetic input: all
+blocks of the workload (default ``c2`` = BASELINE.json configs[1]: two streams
+of 2^28 8-bit ADC samples ~ N(128, 20), 256-bit blocks (q=4, n=64),
+8,388,608 block pairs) in ONE ``bx_extract_eq`` launch on device-resident
+streams.  Inputs (512 MiB) exceed the 126 MB L2, so no flush is needed between
+steps.
+
+Keys beyond the base contract:
+* ``e2e``          the same metric through the public API
+                   (``extract_eq(x, y, plan).run(sink)``) from pinned host
+                   memory: H2D of both streams, the kernel, D2H of the output
+                   and the host bookkeeping, every step;
+* ``roofline``     the kernel's algorithmic bytes / its mean event-timed
+                   duration vs the measured HBM copy peak (MEASURED_PEAKS.json);
+                   ``traffic`` = DRAM bytes per launch from the committed ncu
+                   capture (profiles/ncu_traffic.json) when present;
+* ``cpu_baseline`` the CPU port of the reference algorithm (oracle/, mode 0 =
+                   reduce every product, reference gf2q.py:156-169) on a bounded
+                   prefix, all host threads, rank 0 at N=1 only;
+* ``clocks``       NVML SM clock samples taken during the timed region.
+
+Multi-GPU (torchrun): weak scaling -- every rank runs the full per-GPU
+workload on its own seeded streams (seed + 1000*rank); no collective on the
+data path; the timed region is bracketed by barriers and the reported time is
+the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import io
+import json
+import os
+import pathlib
+import sys
+import threading
+import time
+
+REPO = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "extracted output Gbps and raw input Gbps per GPU at 1/2/4/8 B200; % HBM roofline"
+UNIT = "Gbit/s raw input (both sources, whole job)"
+
+
+def _peaks() -> tuple[float, str]:
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:  # noqa: BLE001
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _traffic(workload: str):
+    p = REPO / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(workload)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML while the timed region runs."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples: list[int] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nv = None
+
+    def _sample(self):
+        nv = self._nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        names = {
+            "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        }
+        for k, bit in names.items():
+            if r & bit:
+                self.reasons.add(k)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                return
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._sample()
+            self._t = threading.Thread(target=self._loop, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                pass
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_rate(wl, x, y, target_s: float, threads: int = 0, mode: int = 0) -> dict:
+    """Time the CPU port of the reference algorithm on a bounded prefix."""
+    from oracle import coracle
+
+    B = wl.block_bits
+    k = 1024
+    t = 0.0
+    while True:  # grow the prefix until one pass takes >= target_s / 4
+        t0 = time.perf_counter()
+        coracle.extract_eq(x, y, wl.q, wl.n, k, mode=mode, nthreads=threads)
+        t = time.perf_counter() - t0
+        if t >= target_s / 4 or k >= wl.num_blocks:
+            break
+        k = min(wl.num_blocks, k * 4)
+    reps = max(1, int(target_s / max(t, 1e-6)))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        coracle.extract_eq(x, y, wl.q, wl.n, k, mode=mode, nthreads=threads)
+    dt = (time.perf_counter() - t0) / reps
+    return {"blocks": k, "seconds_per_pass": dt,
+            "raw_gbps": 2 * B * k / dt / 1e9, "out_gbps": wl.q * k / dt / 1e9,
+            "cores": threads or coracle.threads()}
+
+
+def run_reference(args, wl) -> None:
+    """--impl reference: the reference algorithm's CPU port on the host cores."""
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    from oracle import coracle
+    from paper_2402_14607_b200 import workloads as W
+
+    nthreads = coracle.threads()
+    # a bounded sample of the workload: a prefix of both seeded streams
+    sample_blocks = min(wl.num_blocks, max(1024, int(args.ref_blocks)))
+    nbits = sample_blocks * wl.block_bits
+    samples = -(-nbits // wl.b)
+    if wl.b == 1:
+        samples += (-samples) % 8
+    x = W.stream_bytes_host(wl.x, samples).tobytes()
+    y = W.stream_bytes_host(wl.y, samples).tobytes()
+    for _ in range(args.warmup):
+        coracle.extract_eq(x, y, wl.q, wl.n, sample_blocks, mode=0, nthreads=nthreads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        coracle.extract_eq(x, y, wl.q, wl.n, sample_blocks, mode=0, nthreads=nthreads)
+    dt = (time.perf_counter() - t0) / args.steps
+    raw = 2 * wl.block_bits * sample_blocks / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": raw, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded PCG64, reference generate() semantics)",
+        "config": {"workload": wl.name, "q": wl.q, "n": wl.n, "bits_per_sample": wl.b,
+                   "blocks_per_step": sample_blocks, "note": wl.note},
+        "output_gbps": wl.q * sample_blocks / dt / 1e9,
+        "cpu_baseline": {"value": raw, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "sample": f"first {sample_blocks} blocks of {wl.name} per step",
+                         "cpu": coracle.cpu_model(),
+                         "algorithm": "reference gf2q.py:44-54,156-169 restated in C "
+                                      "(oracle/bx_oracle.c mode 0), OpenMP over block tiles"},
+        "e2e": {"value": raw, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, wl) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_14607_b200 as bx
+    from paper_2402_14607_b200 import _lib, device as D
+    from paper_2402_14607_b200 import workloads as W
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- inputs: seeded host streams (reference generate() semantics)
+    import dataclasses
+    xs = dataclasses.replace(wl.x, seed=wl.x.seed + 1000 * rank)
+    ys = dataclasses.replace(wl.y, seed=wl.y.seed + 1000 * rank)
+    t_gen = time.perf_counter()
+    xh = W.stream_bytes_host(xs, wl.samples)
+    yh = W.stream_bytes_host(ys, wl.samples)
+    t_gen = time.perf_counter() - t_gen
+    nbytes = wl.stream_bytes
+    B = wl.block_bits
+    nblocks = wl.num_blocks
+
+    xd, _ = D.to_device_stream(xh, dev)
+    yd, _ = D.to_device_stream(yh, dev)
+    obytes = (nblocks * wl.q + 7) // 8
+    out = torch.zeros(D.padded_len(obytes), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        D.extract_eq(xd, nbytes, yd, nbytes, wl.q, wl.n, nblocks, out=out, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- parity spot check of this rank's full-size output (sampled blocks)
+    from oracle import coracle
+    host_out = out[:obytes].cpu().numpy().tobytes()
+    rnd = np.random.default_rng(rank)
+    idx = sorted(set([0, nblocks - 1] + rnd.integers(0, nblocks, 64).tolist()))
+    mism = 0
+    for l in idx:
+        lo = l * B // 8
+        hi = -(-((l + 1) * B) // 8)
+        z = coracle.extract_eq(xh[lo:hi].tobytes(), yh[lo:hi].tobytes(), wl.q, wl.n, 1,
+                               x_bit0=l * B % 8, y_bit0=l * B % 8)
+        seg = host_out[l * wl.q // 8:(l * wl.q + wl.q + 7) // 8 + 1]
+        got = (int.from_bytes(seg, "little") >> (l * wl.q % 8)) & ((1 << wl.q) - 1)
+        mism += int(int.from_bytes(z, "little") != got)
+
+    # ---- timed region: K launches on resident inputs
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = _lib.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_step = ms / args.steps
+    raw_gbps = world * 2 * B * nblocks / (ms_step * 1e-3) / 1e9
+    out_gbps = world * wl.q * nblocks / (ms_step * 1e-3) / 1e9
+
+    # ---- roofline of the (single) kernel: algorithmic bytes per launch
+    alg_bytes = nblocks * (2 * B / 8 + wl.q / 8)
+    peak, peak_src = _peaks()
+    achieved = alg_bytes / (ms_step * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": _traffic(wl.name),
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "kernel_ms": ms_step, "kernel": f"bx::eq_kernel<{wl.q}, staged>",
+                "launch": _lib.launch_info(wl.q, wl.n, nblocks)}
+
+    # ---- e2e: public API from pinned host memory, every step H2D + D2H
+    xp = torch.from_numpy(xh).pin_memory()
+    yp = torch.from_numpy(yh).pin_memory()
+    plan = wl.plan()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    sink = io.BytesIO()
+    bx.extract_eq(xp, yp, plan, device=dev).run(sink)  # warm-up
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sink = io.BytesIO()
+        rep = bx.extract_eq(xp, yp, plan, device=dev).run(sink)
+    torch.cuda.synchronize(dev)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_ok = sink.getvalue() == host_out and rep.blocks_completed == nblocks
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r = cpu_reference_rate(wl, xh.tobytes(), yh.tobytes(), args.cpu_seconds)
+        cpu = {"value": r["raw_gbps"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+               "sample": f"first {r['blocks']} blocks of {wl.name} (both streams), "
+                         f"{r['seconds_per_pass']:.2f} s per pass",
+               "algorithm": "oracle/bx_oracle.c mode 0 (reference gf2q.py:44-54,156-169 in C), "
+                            "OpenMP over block tiles",
+               "output_gbps": r["out_gbps"], "cpu": coracle.cpu_model()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": raw_gbps, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded PCG64, reference generate() semantics; per-rank seeds)",
+            "config": {"workload": wl.name, "q": wl.q, "n": wl.n, "bits_per_sample": wl.b,
+                       "samples_per_stream": wl.samples, "blocks_per_gpu": nblocks,
+                       "input_bytes_per_gpu": 2 * nbytes,
+                       "l2": "inputs exceed the 126 MB L2 (no flush needed)",
+                       "parallelism": f"dp{world} (contiguous block ranges, no collective)",
+                       "note": wl.note},
+            "output_gbps": out_gbps,
+            "raw_gbps_per_gpu": raw_gbps / world,
+            "output_gbps_per_gpu": out_gbps / world,
+            "e2e": {"value": world * 2 * B * nblocks / e2e_s / 1e9, "unit": UNIT,
+                    "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": obytes,
+                    "output_gbps": world * wl.q * nblocks / e2e_s / 1e9,
+                    "seconds_per_step": e2e_s, "steps": e2e_steps,
+                    "path": "paper_2402_14607_b200.extract_eq(pinned host tensors).run(BytesIO)",
+                    "bit_exact_vs_device_run": e2e_ok},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": sampler.summary(),
+            "gpu_launches": launches,
+            "parity": {"sampled_blocks": len(idx), "mismatches": mism},
+            "input_generation_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main(argv=None) -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-blocks", type=int, default=200_000)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args(argv)
+    from paper_2402_14607_b200 import workloads as W
+
+    wl = W.WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

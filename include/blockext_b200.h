@@ -1,0 +1,90 @@
+/*
+ * blockext_b200.h -- C ABI of the B200 block extractor (libbx_b200.so).
+ *
+ * Plain pointers and sizes only.  Every compute entry point is asynchronous on
+ * the given cudaStream_t (passed as void*, NULL = legacy default stream) and
+ * returns 0 on success or a negative BX_E* code; bx_last_error() then holds a
+ * thread-local message.  All buffers are device buffers owned by the caller;
+ * the library keeps no allocations between calls.
+ *
+ * The reference (`blockext`, pure Python) has no FFI; these entry points
+ * replace the compute of its Python functions, which the package
+ * paper_2402_14607_b200 re-exposes with the reference's signatures:
+ *
+ *   bx_extract_eq   <- Extraction._blocks + run_parallel + ext_ip + GFContext.mul
+ *                      + BitWriter      (pkg/src/blockext/extractor.py:182-208,
+ *                      :94-130, :77-87; gf2q.py:156-169; bitio.py:67-88)
+ *   bx_pack         <- sources._pack_samples (pkg/src/blockext/sources.py:116-121)
+ *                      and the bit packing inside generate() (:133-140)
+ *   bx_modulus_exponents <- _moduli.MODULUS_EXPONENTS / modulus_int
+ *                      (pkg/src/blockext/_moduli.py:13-151)
+ */
+#ifndef BLOCKEXT_B200_H
+#define BLOCKEXT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BX_OK 0
+#define BX_EINVAL -1   /* bad argument (message says which)            */
+#define BX_ECUDA -2    /* CUDA launch/runtime error                      */
+#define BX_ERANGE -3   /* field width outside 1..128 (reference CapacityError) */
+
+/* ABI version (major*100 + minor). */
+int bx_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* bx_last_error(void);
+
+/* Default modulus of GF(2^q): writes its exponents, highest first, to exps[5]
+ * and returns how many there are (2, 3 or 5); BX_ERANGE for q outside 1..128. */
+int bx_modulus_exponents(int q, int* exps);
+
+/*
+ * Equal-width two-source extraction of `nblocks` blocks.
+ *
+ * Block l reads bits [x_bit0 + l*q*n, x_bit0 + (l+1)*q*n) of the LSB-first bit
+ * stream at x (and likewise y), splits them into n q-bit elements and writes
+ *   z_l = sum_j x_{l,j} * y_{l,j}  in GF(2^q) (default modulus)
+ * to bits [out_bit0 + l*q, out_bit0 + (l+1)*q) of out.  Other bits of out are
+ * preserved (boundary words are updated atomically).
+ *
+ * x, y, out: device pointers, 4-byte aligned.  x_bytes / y_bytes: bytes of
+ * valid stream data; the buffers must stay readable up to the next multiple of
+ * 4 bytes plus 4 more.  Requires x_bit0 + nblocks*q*n <= 8*x_bytes (same for y).
+ */
+int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0,
+                  const void* y, int64_t y_bytes, int64_t y_bit0,
+                  int q, int n, int64_t nblocks,
+                  void* out, int64_t out_bit0, void* stream);
+
+/*
+ * Launch geometry bx_extract_eq would use (for tests, benches and profiling):
+ * threads per block-pair group, blocks per CTA tile, staged (1) or direct (0),
+ * CTA threads, dynamic shared memory bytes, grid size, and kernel family
+ * (0 = diag, 1 = holes).  Any output pointer may be NULL.
+ */
+int bx_launch_info(int q, int n, int64_t nblocks, int* tpb, int* tile, int* staged,
+                   int* threads, int* smem_bytes, int64_t* grid, int* family);
+
+/*
+ * Sample packer: the low b bits of sample i go to stream bits
+ * [out_bit0 + i*b, out_bit0 + (i+1)*b).  samples: `count` little-endian
+ * unsigned integers of elem_bytes (1, 2, 4 or 8) each; b in 1..8*elem_bytes.
+ * Bits of out outside the written range are preserved; out must be 4-byte
+ * aligned.
+ */
+int bx_pack(const void* samples, int elem_bytes, int b, int64_t count,
+            void* out, int64_t out_bit0, void* stream);
+
+/* Number of kernel launches issued by this thread since the last reset. */
+int64_t bx_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BLOCKEXT_B200_H */

@@ -1,0 +1,88 @@
+"""ctypes binding of libbx_b200.so (the sm_100a kernels behind include/blockext_b200.h).
+
+There is no CPU fallback: if the library is missing or cannot be loaded every
+product entry point raises :class:`ExtensionMissingError`.
+"""
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import threading
+
+from .errors import CapacityError, DeviceError, ExtensionMissingError
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "libbx_b200.so"
+
+BX_OK, BX_EINVAL, BX_ECUDA, BX_ERANGE = 0, -1, -2, -3
+
+#: symbol -> (restype, argtypes); mirrors include/blockext_b200.h exactly
+_i32, _i64, _vp, _cp = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_char_p
+_PI32, _PI64 = ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64)
+SIGNATURES = {
+    "bx_version": (_i32, []),
+    "bx_last_error": (_cp, []),
+    "bx_modulus_exponents": (_i32, [_i32, _PI32]),
+    "bx_extract_eq": (_i32, [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i64, _vp, _i64, _vp]),
+    "bx_launch_info": (_i32, [_i32, _i32, _i64, _PI32, _PI32, _PI32, _PI32, _PI32, _PI64, _PI32]),
+    "bx_pack": (_i32, [_vp, _i32, _i32, _i64, _vp, _i64, _vp]),
+    "bx_launch_count": (_i64, [_i32]),
+}
+
+_lock = threading.Lock()
+_handle = None
+
+
+def lib():
+    """The loaded library (loaded once); raises ExtensionMissingError if absent."""
+    global _handle
+    if _handle is not None:
+        return _handle
+    with _lock:
+        if _handle is None:
+            if not LIB_PATH.exists():
+                raise ExtensionMissingError(
+                    f"{LIB_PATH} is not built; run `python -m paper_2402_14607_b200.build` "
+                    "(there is no CPU fallback)")
+            try:
+                h = ctypes.CDLL(str(LIB_PATH))
+            except OSError as exc:
+                raise ExtensionMissingError(f"cannot load {LIB_PATH}: {exc}") from exc
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(h, name)
+                fn.restype = res
+                fn.argtypes = args
+            _handle = h
+    return _handle
+
+
+def check(rc: int, what: str) -> int:
+    if rc >= 0:
+        return rc
+    msg = lib().bx_last_error().decode(errors="replace")
+    if rc == BX_ERANGE:
+        raise CapacityError(f"{what}: {msg}")
+    if rc == BX_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    raise DeviceError(f"{what}: {msg}")
+
+
+def modulus_exponents(q: int) -> tuple[int, ...]:
+    buf = (ctypes.c_int * 5)()
+    cnt = check(lib().bx_modulus_exponents(q, buf), "bx_modulus_exponents")
+    return tuple(buf[:cnt])
+
+
+def launch_info(q: int, n: int, nblocks: int) -> dict:
+    vals = [ctypes.c_int() for _ in range(6)]
+    grid = ctypes.c_int64()
+    fam = ctypes.c_int()
+    check(lib().bx_launch_info(q, n, nblocks, *[ctypes.byref(v) for v in vals[:5]],
+                               ctypes.byref(grid), ctypes.byref(fam)), "bx_launch_info")
+    tpb, tile, staged, threads, smem = (v.value for v in vals[:5])
+    return {"tpb": tpb, "tile": tile, "staged": staged, "threads": threads,
+            "smem_bytes": smem, "grid": grid.value,
+            "family": "diag" if fam.value == 0 else "holes"}
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib().bx_launch_count(1 if reset else 0))

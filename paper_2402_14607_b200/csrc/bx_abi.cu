@@ -1,0 +1,131 @@
+// bx_abi.cu -- the extern "C" boundary (include/blockext_b200.h).
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <utility>
+
+#include <cuda_runtime.h>
+
+#include "../../include/blockext_b200.h"
+#include "bx_launch.cuh"
+
+namespace bx {
+cudaError_t launch_pack(const void*, int, int, int64_t, void*, int64_t, cudaStream_t);
+
+#define BX_EXTERN_Q(Q) extern template cudaError_t launch_eq<Q>(const EqArgs&, const LaunchCfg&, cudaStream_t);
+#define BX_X8(b) BX_EXTERN_Q(b + 1) BX_EXTERN_Q(b + 2) BX_EXTERN_Q(b + 3) BX_EXTERN_Q(b + 4) \
+                 BX_EXTERN_Q(b + 5) BX_EXTERN_Q(b + 6) BX_EXTERN_Q(b + 7) BX_EXTERN_Q(b + 8)
+BX_X8(0) BX_X8(8) BX_X8(16) BX_X8(24) BX_X8(32) BX_X8(40) BX_X8(48) BX_X8(56)
+BX_X8(64) BX_X8(72) BX_X8(80) BX_X8(88) BX_X8(96) BX_X8(104) BX_X8(112) BX_X8(120)
+
+template <int... Is>
+constexpr auto make_table(std::integer_sequence<int, Is...>) {
+  return std::array<LaunchFn, sizeof...(Is)>{{&launch_eq<Is + 1>...}};
+}
+}  // namespace bx
+
+#include <array>
+
+namespace {
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+const std::array<bx::LaunchFn, 128>& table() {
+  static const auto t = bx::make_table(std::make_integer_sequence<int, 128>{});
+  return t;
+}
+}  // namespace
+
+extern "C" {
+
+int bx_version(void) { return 100; }
+
+const char* bx_last_error(void) { return g_err.c_str(); }
+
+int bx_modulus_exponents(int q, int* exps) {
+  if (q < 1 || q > 128) return fail(BX_ERANGE, "field width outside 1..128");
+  const bx::ModRow& r = bx::kModulus[q];
+  for (int i = 0; i < 5; i++) exps[i] = i < r.count ? r.e[i] : 0;
+  return r.count;
+}
+
+int bx_launch_info(int q, int n, int64_t nblocks, int* tpb, int* tile, int* staged,
+                   int* threads, int* smem_bytes, int64_t* grid, int* family) {
+  if (q < 1 || q > 128) return fail(BX_ERANGE, "field width outside 1..128");
+  if (n < 1 || nblocks < 0) return fail(BX_EINVAL, "n must be >= 1 and nblocks >= 0");
+  const bx::LaunchCfg c = bx::choose_launch(q, n, nblocks);
+  if (tpb) *tpb = 1 << c.tpb_log2;
+  if (tile) *tile = c.tile;
+  if (staged) *staged = c.staged;
+  if (threads) *threads = c.threads;
+  if (smem_bytes) *smem_bytes = (int)c.smem;
+  if (grid) *grid = c.grid;
+  if (family) *family = c.family;
+  return BX_OK;
+}
+
+int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0, const void* y, int64_t y_bytes,
+                  int64_t y_bit0, int q, int n, int64_t nblocks, void* out, int64_t out_bit0,
+                  void* stream) {
+  if (q < 1 || q > 128) return fail(BX_ERANGE, "field width outside 1..128");
+  if (n < 1) return fail(BX_EINVAL, "vec_len must be >= 1");
+  if (nblocks < 0 || x_bit0 < 0 || y_bit0 < 0 || out_bit0 < 0 || x_bytes < 0 || y_bytes < 0)
+    return fail(BX_EINVAL, "negative size or offset");
+  if (nblocks == 0) return BX_OK;
+  if (!x || !y || !out) return fail(BX_EINVAL, "null buffer");
+  if (((uintptr_t)x | (uintptr_t)y | (uintptr_t)out) & 3)
+    return fail(BX_EINVAL, "buffers must be 4-byte aligned");
+  const int64_t B = (int64_t)q * n;
+  if (nblocks > (INT64_MAX - x_bit0) / B || nblocks > (INT64_MAX - y_bit0) / B)
+    return fail(BX_EINVAL, "block range overflows");
+  if (x_bit0 + nblocks * B > 8 * x_bytes) return fail(BX_EINVAL, "x stream shorter than the block range");
+  if (y_bit0 + nblocks * B > 8 * y_bytes) return fail(BX_EINVAL, "y stream shorter than the block range");
+  const bx::LaunchCfg c = bx::choose_launch(q, n, nblocks);
+  if (c.grid > 0x7FFFFFFF) return fail(BX_EINVAL, "too many blocks for one launch");
+  bx::EqArgs a;
+  a.x = static_cast<const uint32_t*>(x);
+  a.y = static_cast<const uint32_t*>(y);
+  a.x_bit0 = x_bit0;
+  a.y_bit0 = y_bit0;
+  a.x_words = (x_bytes + 3) / 4;
+  a.y_words = (y_bytes + 3) / 4;
+  a.nblocks = nblocks;
+  a.out = static_cast<uint32_t*>(out);
+  a.out_bit0 = out_bit0;
+  a.n = n;
+  a.tpb_log2 = c.tpb_log2;
+  a.tile_blocks = c.tile;
+  a.stage_words = c.stage_words;
+  cudaError_t e = table()[q - 1](a, c, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_extract_eq: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int bx_pack(const void* samples, int elem_bytes, int b, int64_t count, void* out, int64_t out_bit0,
+            void* stream) {
+  if (!(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8))
+    return fail(BX_EINVAL, "elem_bytes must be 1, 2, 4 or 8");
+  if (b < 1 || b > 8 * elem_bytes) return fail(BX_EINVAL, "bits per sample outside 1..8*elem_bytes");
+  if (count < 0 || out_bit0 < 0) return fail(BX_EINVAL, "negative count or offset");
+  if (count == 0) return BX_OK;
+  if (!samples || !out) return fail(BX_EINVAL, "null buffer");
+  if ((uintptr_t)out & 3) return fail(BX_EINVAL, "out must be 4-byte aligned");
+  cudaError_t e = bx::launch_pack(samples, elem_bytes, b, count, out, out_bit0,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_pack: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int64_t bx_launch_count(int reset) {
+  return reset ? g_launches.exchange(0) : g_launches.load();
+}
+
+}  // extern "C"

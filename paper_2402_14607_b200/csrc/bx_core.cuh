@@ -1,0 +1,388 @@
+// bx_core.cuh -- GF(2^q) block inner-product kernels for sm_100a.
+//
+// One block l of an equal-width run reads q*n bits of each stream,
+// x_l = bits [x_bit0 + l*q*n, ...), y_l likewise, splits them into n q-bit
+// elements LSB-first (reference extractor.py:182-208, bitio.py:45-60) and emits
+//
+//     z_l = reduce_P( XOR_j clmul(x_lj, y_lj) )                       (*)
+//
+// at output bits [out_bit0 + l*q, ...) (reference bitio.py:74-88).  (*) equals
+// the reference's XOR of reduced products (extractor.py:77-87 with
+// gf2q.py:156-169) because reduction mod P is GF(2)-linear; the carry-less
+// products are therefore accumulated UNREDUCED over the block and reduced once.
+//
+// There is no carry-less multiply instruction on the GPU.  Two integer-pipe
+// formulations are used, chosen at compile time by Q:
+//
+//  * Diag (Q <= 8): a 32-bit chunk holds E = 32/Q elements.  For every shift
+//    d in (-Q, Q):  acc_d ^= (X >> d) & Y   (X << -d for d < 0).  Bit jQ+b of
+//    acc_d accumulates x_{j,b+d} * y_{j,b}; at the end
+//        c_k = XOR_{b} parity(acc_{k-2b} & M_b),   M_b = {jQ+b : j < E}.
+//    Cost: 2Q-1 LOP3 + 2Q-2 shifts per chunk of E elements (ALU + IMAD.SHL).
+//
+//  * Holes (Q >= 9): elements are cut into 16-bit halves; a 16x16 carry-less
+//    product is formed with nine 32-bit IMADs on "holed" operands
+//    (bits = i mod 3 of each half).  In each integer product all set
+//    coefficients sit at positions = (i+k) mod 3 and each coefficient count is
+//    <= 6 < 8, so no carry reaches the next same-residue position: bit p of the
+//    product is the parity of the count, i.e. the carry-less coefficient.
+//    Products are XOR-accumulated per (slot, residue) and masked once per block.
+//    IMAD.WIDE is avoided: it issues at 1/3 the rate of IMAD on sm_100a
+//    (profiles/r01_pipes_microbench.txt).
+//
+// Reduction mod P uses the shipped sparse modulus (bx_moduli.h) with all shift
+// amounts compile-time constants.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "bx_moduli.h"
+
+namespace bx {
+
+constexpr int kDiagMaxQ = 8;
+
+__host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// ----------------------------------------------------------- multiword values
+
+template <int N>
+struct Wide {
+  uint32_t w[N];
+};
+
+template <int N>
+__device__ __forceinline__ uint32_t at(const Wide<N>& a, int i) {
+  return (i >= 0 && i < N) ? a.w[i] : 0u;
+}
+
+template <int N>
+__device__ __forceinline__ Wide<N> wzero() {
+  Wide<N> r;
+#pragma unroll
+  for (int i = 0; i < N; i++) r.w[i] = 0u;
+  return r;
+}
+
+// r = a >> S, truncated to M words
+template <int S, int M, int N>
+__device__ __forceinline__ Wide<M> wshr(const Wide<N>& a) {
+  Wide<M> r;
+  constexpr int ws = S / 32, bs = S % 32;
+#pragma unroll
+  for (int i = 0; i < M; i++) {
+    const uint32_t lo = at(a, i + ws), hi = at(a, i + ws + 1);
+    r.w[i] = bs ? __funnelshift_r(lo, hi, bs) : lo;
+  }
+  return r;
+}
+
+// r ^= a << S (r has M words, bits shifted past M words are dropped)
+template <int S, int M, int N>
+__device__ __forceinline__ void wxor_shl(Wide<M>& r, const Wide<N>& a) {
+  constexpr int ws = S / 32, bs = S % 32;
+#pragma unroll
+  for (int i = 0; i < M; i++) {
+    const uint32_t hi = at(a, i - ws), lo = at(a, i - ws - 1);
+    r.w[i] ^= bs ? __funnelshift_l(lo, hi, bs) : hi;
+  }
+}
+
+// low Q bits of a, as cdiv(Q,32) words
+template <int Q, int N>
+__device__ __forceinline__ Wide<cdiv(Q, 32)> wlow(const Wide<N>& a) {
+  constexpr int M = cdiv(Q, 32);
+  Wide<M> r;
+#pragma unroll
+  for (int i = 0; i < M; i++) r.w[i] = at(a, i);
+  if constexpr (Q % 32) r.w[M - 1] &= (1u << (Q % 32)) - 1u;
+  return r;
+}
+
+// ------------------------------------------------------- reduction mod P(Q)
+
+__host__ __device__ constexpr int fold_rounds(int q) {
+  // c has degree <= 2q-2, so its high part (c >> q) has degree <= q-2.  One
+  // fold maps a high part of degree d to one of degree d + e_max - q.
+  int emax = 0;
+  for (int i = 1; i < kModulus[q].count; i++)
+    if (kModulus[q].e[i] > emax) emax = kModulus[q].e[i];
+  int d = q - 2, f = 0;
+  while (d >= 0) {
+    d += emax - q;
+    f++;
+  }
+  return f;
+}
+
+template <int Q, int I, int CW>
+__device__ __forceinline__ void fold_terms(Wide<CW>& t, const Wide<CW>& hi) {
+  if constexpr (I < kModulus[Q].count) {
+    constexpr int e = kModulus[Q].e[I];
+    if constexpr (e != Q) wxor_shl<e>(t, hi);
+    fold_terms<Q, I + 1, CW>(t, hi);
+  }
+}
+
+// z = c mod P, c of degree <= 2Q-2 held in CW words
+template <int Q, int CW>
+__device__ __forceinline__ Wide<cdiv(Q, 32)> reduce(const Wide<CW>& c) {
+  Wide<cdiv(Q, 32)> lo = wlow<Q>(c);
+  Wide<CW> hi = wshr<Q, CW>(c);
+  constexpr int F = fold_rounds(Q);
+#pragma unroll
+  for (int f = 0; f < F; f++) {
+    Wide<CW> t = wzero<CW>();
+    fold_terms<Q, 0, CW>(t, hi);
+    const Wide<cdiv(Q, 32)> tl = wlow<Q>(t);
+#pragma unroll
+    for (int i = 0; i < cdiv(Q, 32); i++) lo.w[i] ^= tl.w[i];
+    hi = wshr<Q, CW>(t);
+  }
+  return lo;
+}
+
+// --------------------------------------------------------------- bit access
+
+// 32 bits of an LSB-first word stream starting at bit `off` (word off>>5 + 1
+// must be readable).
+__device__ __forceinline__ uint32_t read32(const uint32_t* src, int64_t off) {
+  const int64_t w = off >> 5;
+  return __funnelshift_r(src[w], src[w + 1], (uint32_t)(off & 31));
+}
+
+// ------------------------------------------------------------- diag (Q<=8)
+
+template <int Q>
+struct Diag {
+  static constexpr int E = 32 / Q;   // elements per 32-bit chunk
+  static constexpr int EB = E * Q;   // bits per chunk
+  uint32_t pos[Q];                   // d = 0 .. Q-1
+  uint32_t neg[Q];                   // d = -1 .. -(Q-1) at index 1 .. Q-1
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int d = 0; d < Q; d++) pos[d] = neg[d] = 0u;
+  }
+
+  __device__ __forceinline__ void add(uint32_t X, uint32_t Y) {
+#pragma unroll
+    for (int d = 0; d < Q; d++) pos[d] ^= (X >> d) & Y;
+#pragma unroll
+    for (int d = 1; d < Q; d++) neg[d] ^= (X << d) & Y;
+  }
+
+  static __host__ __device__ constexpr uint32_t mask_b(int b) {
+    uint32_t m = 0;
+    for (int j = 0; j < E; j++) m |= 1u << (j * Q + b);
+    return m;
+  }
+
+  // unreduced c (2Q-1 <= 15 bits)
+  __device__ __forceinline__ uint32_t unreduced() const {
+    uint32_t c = 0;
+#pragma unroll
+    for (int b = 0; b < Q; b++) {
+#pragma unroll
+      for (int a = 0; a < Q; a++) {
+        const int d = a - b;
+        const uint32_t acc = d >= 0 ? pos[d] : neg[-d];
+        c ^= (uint32_t)(__popc(acc & mask_b(b)) & 1) << (a + b);
+      }
+    }
+    return c;
+  }
+};
+
+// ---------------------------------------------------------- holes (Q >= 9)
+
+template <int Q>
+struct Holes {
+  static constexpr int EW = cdiv(Q, 32);       // 32-bit words per element
+  static constexpr int NH = cdiv(Q, 16);       // 16-bit halves per element
+  static constexpr int NS = 2 * NH - 1;        // half-product slots
+  static constexpr int CW = cdiv(2 * Q - 1, 32);
+  uint32_t acc[NS][3];
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int s = 0; s < NS; s++) acc[s][0] = acc[s][1] = acc[s][2] = 0u;
+  }
+
+  __device__ __forceinline__ void add(const uint32_t (&xw)[EW], const uint32_t (&yw)[EW]) {
+    uint32_t xs[NH][3], ys[NH][3];
+#pragma unroll
+    for (int u = 0; u < NH; u++) {
+      const uint32_t xh = (xw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+      const uint32_t yh = (yw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+      xs[u][0] = xh & 0x9249u; xs[u][1] = xh & 0x2492u; xs[u][2] = xh & 0x4924u;
+      ys[u][0] = yh & 0x9249u; ys[u][1] = yh & 0x2492u; ys[u][2] = yh & 0x4924u;
+    }
+#pragma unroll
+    for (int u = 0; u < NH; u++) {
+#pragma unroll
+      for (int v = 0; v < NH; v++) {
+        // residue r collects (i, k) with i + k = r (mod 3)
+        acc[u + v][0] ^= (xs[u][0] * ys[v][0]) ^ (xs[u][1] * ys[v][2]) ^ (xs[u][2] * ys[v][1]);
+        acc[u + v][1] ^= (xs[u][0] * ys[v][1]) ^ (xs[u][1] * ys[v][0]) ^ (xs[u][2] * ys[v][2]);
+        acc[u + v][2] ^= (xs[u][0] * ys[v][2]) ^ (xs[u][1] * ys[v][1]) ^ (xs[u][2] * ys[v][0]);
+      }
+    }
+  }
+
+  __device__ __forceinline__ Wide<CW> unreduced() const {
+    Wide<CW> c = wzero<CW>();
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+      const uint32_t cs = (acc[s][0] & 0x49249249u) | (acc[s][1] & 0x92492492u) |
+                          (acc[s][2] & 0x24924924u);
+      placed_xor(c, cs, s);  // slot s sits at bit 16*s; cs has <= 31 bits
+    }
+    return c;
+  }
+
+  static __device__ __forceinline__ void placed_xor(Wide<CW>& c, uint32_t cs, int s) {
+    // xor cs << (16*s) into c; s is a compile-time constant after unrolling
+    const int w = (16 * s) >> 5;
+    if ((s & 1) == 0) {
+      if (w < CW) c.w[w] ^= cs;
+    } else {
+      if (w < CW) c.w[w] ^= cs << 16;
+      if (w + 1 < CW) c.w[w + 1] ^= cs >> 16;
+    }
+  }
+};
+
+// ----------------------------------------------------------------- kernel
+
+struct EqArgs {
+  const uint32_t* x;
+  const uint32_t* y;
+  int64_t x_bit0;
+  int64_t y_bit0;
+  int64_t x_words;     // readable words of x (bounds for staging)
+  int64_t y_words;
+  int64_t nblocks;
+  uint32_t* out;
+  int64_t out_bit0;
+  int n;
+  int tpb_log2;        // threads per block = 1 << tpb_log2 (<= 32)
+  int tile_blocks;     // blocks per CTA
+  int stage_words;     // smem words per source (STAGED only)
+};
+
+template <int Q, int EW>
+__device__ __forceinline__ void read_elem(const uint32_t* src, int64_t off, uint32_t (&w)[EW]) {
+#pragma unroll
+  for (int i = 0; i < EW; i++) w[i] = read32(src, off + 32 * i);
+  if constexpr (Q % 32) w[EW - 1] &= (1u << (Q % 32)) - 1u;
+}
+
+template <int Q, bool STAGED>
+__global__ void __launch_bounds__(256) eq_kernel(const EqArgs a) {
+  extern __shared__ uint32_t smem[];
+  constexpr int EW = cdiv(Q, 32);
+  constexpr int CW = cdiv(2 * Q - 1, 32);
+  const int tpb = 1 << a.tpb_log2;
+  const int T = a.tile_blocks;
+  const int64_t B = (int64_t)Q * a.n;
+  const int64_t tile0 = (int64_t)blockIdx.x * T;
+  const int nb = (int)((a.nblocks - tile0) < T ? (a.nblocks - tile0) : T);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int grp = tid >> a.tpb_log2, sub = tid & (tpb - 1);
+
+  const uint32_t* sx;
+  const uint32_t* sy;
+  uint32_t* so;
+  int64_t xbase, ybase;
+  if constexpr (STAGED) {
+    const int sw = a.stage_words;
+    const int64_t xs = a.x_bit0 + tile0 * B, ys = a.y_bit0 + tile0 * B;
+    const int64_t xw0 = xs >> 5, yw0 = ys >> 5;
+    const int nwx = (int)((((xs & 31) + nb * B + 31) >> 5) + 1);
+    const int nwy = (int)((((ys & 31) + nb * B + 31) >> 5) + 1);
+    for (int i = tid; i < nwx; i += nthr)
+      smem[i] = (xw0 + i < a.x_words) ? __ldg(a.x + xw0 + i) : 0u;
+    for (int i = tid; i < nwy; i += nthr)
+      smem[sw + i] = (yw0 + i < a.y_words) ? __ldg(a.y + yw0 + i) : 0u;
+    sx = smem;
+    sy = smem + sw;
+    so = smem + 2 * sw;
+    xbase = xs & 31;
+    ybase = ys & 31;
+  } else {
+    sx = a.x;
+    sy = a.y;
+    so = smem;
+    xbase = a.x_bit0 + tile0 * B;
+    ybase = a.y_bit0 + tile0 * B;
+  }
+  const int64_t ostart = a.out_bit0 + tile0 * Q;
+  const int ow = (int)((((ostart & 31) + (int64_t)nb * Q + 31) >> 5));
+  for (int i = tid; i < ow + 1; i += nthr) so[i] = 0u;
+  __syncthreads();
+
+  Wide<CW> c = wzero<CW>();
+  if (grp < nb) {
+    const int64_t xo = xbase + grp * B, yo = ybase + grp * B;
+    if constexpr (Q <= kDiagMaxQ) {
+      using D = Diag<Q>;
+      D acc;
+      acc.init();
+      const int nch = cdiv(a.n, D::E);
+      for (int ch = sub; ch < nch; ch += tpb) {
+        const int64_t off = (int64_t)ch * D::EB;
+        const int valid = min(D::E, a.n - ch * D::E) * Q;
+        const uint32_t m = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+        acc.add(read32(sx, xo + off) & m, read32(sy, yo + off));
+      }
+      c.w[0] = acc.unreduced();
+    } else {
+      Holes<Q> acc;
+      acc.init();
+      for (int j = sub; j < a.n; j += tpb) {
+        uint32_t xw[EW], yw[EW];
+        read_elem<Q>(sx, xo + (int64_t)j * Q, xw);
+        read_elem<Q>(sy, yo + (int64_t)j * Q, yw);
+        acc.add(xw, yw);
+      }
+      c = acc.unreduced();
+    }
+  }
+  for (int m = 1; m < tpb; m <<= 1) {
+#pragma unroll
+    for (int i = 0; i < CW; i++) c.w[i] ^= __shfl_xor_sync(0xFFFFFFFFu, c.w[i], m);
+  }
+  if (grp < nb && sub == 0) {
+    const Wide<EW> z = reduce<Q>(c);
+    const int64_t ob = (ostart & 31) + (int64_t)grp * Q;
+    const int w0 = (int)(ob >> 5);
+    const uint32_t sh = (uint32_t)(ob & 31);
+#pragma unroll
+    for (int i = 0; i <= EW; i++) {
+      const uint32_t lo = at(z, i - 1), hi = at(z, i);
+      const uint32_t v = sh ? __funnelshift_l(lo, hi, sh) : hi;
+      if (v) atomicOr(&so[w0 + i], v);
+    }
+  }
+  __syncthreads();
+  const int64_t gw0 = ostart >> 5;
+  const int64_t oend = ostart + (int64_t)nb * Q;
+  for (int i = tid; i < ow; i += nthr) {
+    const int64_t lo = (gw0 + i) * 32, hi = lo + 32;
+    const uint32_t v = so[i];
+    if (lo >= ostart && hi <= oend) {
+      a.out[gw0 + i] = v;
+    } else {
+      const int64_t s = lo > ostart ? lo : ostart;
+      const int64_t e = hi < oend ? hi : oend;
+      const int nbits = (int)(e - s), off = (int)(s - lo);
+      const uint32_t mask = (nbits >= 32 ? 0xFFFFFFFFu : ((1u << nbits) - 1u)) << off;
+      atomicAnd(&a.out[gw0 + i], ~mask);
+      atomicOr(&a.out[gw0 + i], v & mask);
+    }
+  }
+}
+
+}  // namespace bx

@@ -1,0 +1,94 @@
+"""Device-buffer layer over the C ABI: torch tensors as HBM buffers, CUDA streams.
+
+PyTorch is plumbing here (allocation, streams, copies); all compute is the
+sm_100a library.  Stream buffers are uint8 tensors padded so the kernels may
+read whole 32-bit words plus one guard word past the last stream bit.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DeviceError
+
+PAD_BYTES = 16
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the extractor runs only on the sm_100a kernels")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise DeviceError(f"device {d} is not a CUDA device")
+    return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def padded_len(nbytes: int) -> int:
+    return ((nbytes + 15) // 16) * 16 + PAD_BYTES
+
+
+def empty_stream(nbytes: int, device, zero_pad: bool = True) -> torch.Tensor:
+    """uint8 device buffer for `nbytes` of stream data plus the guard padding."""
+    t = torch.empty(padded_len(nbytes), dtype=torch.uint8, device=device)
+    if zero_pad:
+        t[nbytes:].zero_()
+    return t
+
+
+def to_device_stream(data, device, pin: bool = False) -> tuple[torch.Tensor, int]:
+    """Copy host bytes-like / numpy / torch data into a padded device buffer."""
+    if isinstance(data, torch.Tensor):
+        src = data.reshape(-1).view(torch.uint8)
+    else:
+        arr = np.frombuffer(memoryview(data), dtype=np.uint8) if not isinstance(data, np.ndarray) \
+            else np.ascontiguousarray(data).reshape(-1).view(np.uint8)
+        src = torch.from_numpy(arr) if arr.size else torch.empty(0, dtype=torch.uint8)
+        if pin and src.numel():
+            src = src.pin_memory()
+    n = src.numel()
+    buf = empty_stream(n, device)
+    if n:
+        buf[:n].copy_(src, non_blocking=pin)
+    return buf, n
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None, device=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return int(s.cuda_stream)
+
+
+def extract_eq(x: torch.Tensor, x_bytes: int, y: torch.Tensor, y_bytes: int, q: int, n: int,
+               nblocks: int, *, x_bit0: int = 0, y_bit0: int = 0, out: torch.Tensor | None = None,
+               out_bit0: int = 0, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Launch bx_extract_eq on device buffers; returns the (padded) output buffer."""
+    if out is None:
+        nbytes = (out_bit0 + nblocks * q + 7) // 8
+        out = torch.zeros(padded_len(nbytes), dtype=torch.uint8, device=x.device)
+    for t in (x, y, out):
+        if not t.is_cuda or t.dtype != torch.uint8 or not t.is_contiguous():
+            raise ValueError("device buffers must be contiguous uint8 CUDA tensors")
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.lib().bx_extract_eq(
+            x.data_ptr(), x_bytes, x_bit0, y.data_ptr(), y_bytes, y_bit0, q, n, nblocks,
+            out.data_ptr(), out_bit0, stream_ptr(stream, x.device)), "bx_extract_eq")
+    return out
+
+
+def pack(samples: torch.Tensor, b: int, *, out: torch.Tensor | None = None, out_bit0: int = 0,
+         stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Pack the low b bits of each sample LSB-first (reference sources.py:116-121)."""
+    elem = samples.element_size()
+    if elem not in (1, 2, 4, 8) or samples.is_floating_point():
+        raise ValueError("samples must be an integer tensor of 1, 2, 4 or 8 byte elements")
+    count = samples.numel()
+    if out is None:
+        end = out_bit0 + count * b
+        out = empty_stream((end + 7) // 8, samples.device)
+        out[(end // 32) * 4:].zero_()   # zero pad bits of the last word (bitio.py:84-88)
+    with torch.cuda.device(samples.device):
+        _lib.check(_lib.lib().bx_pack(samples.data_ptr(), elem, b, count, out.data_ptr(), out_bit0,
+                                      stream_ptr(stream, samples.device)), "bx_pack")
+    return out

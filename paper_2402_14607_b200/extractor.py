@@ -1,0 +1,547 @@
+"""Streaming two-source extraction with the reference's API, computed on B200.
+
+Drop-in for ``blockext.extractor`` (reference pkg/src/blockext/extractor.py):
+same names, parameters, output bit layout, report accounting and errors.  What
+changes is where the work happens:
+
+* framing, the GF(2^q) inner products and the output packing of every block
+  run in one sm_100a kernel launch per segment (``bx_extract_eq``);
+* the host keeps only the bookkeeping of the reference's ``BitReader``
+  (bitio.py:25-64): it replays the exact sequence of ``read(size)`` calls the
+  reference would make on each stream, in bulk, so ``*_bits_consumed``,
+  ``*_discarded_tail_bits`` and the stop reason match bit for bit without a
+  per-block Python loop.
+
+Segments of up to ``segment_blocks`` blocks (a multiple of 64, so every segment
+starts on a byte boundary of the inputs and of the output) bound host and
+device memory on long or unbounded inputs.
+"""
+from __future__ import annotations
+
+import io
+import time
+from dataclasses import dataclass
+from typing import Iterable, Iterator, Sequence
+
+import numpy as np
+
+from . import params as _params
+from .gf2q import MAX_FIELD_BITS, GFContext, field
+from .params import error_bound_eq, error_bound_neq
+from .report import ExtractionReport
+
+READ_CHUNK = 1 << 16          # BitReader chunk size (reference bitio.py:25)
+DEFAULT_SEGMENT_BLOCKS = 1 << 24
+
+
+@dataclass(frozen=True)
+class OutputChunk:
+    """One block's output: `width` bits, emitted in block order."""
+
+    index: int   # 1-based block index
+    bits: int
+    width: int
+
+
+@dataclass(frozen=True)
+class BlockPair:
+    """The paired input windows of one block, as field-element vectors."""
+
+    index: int
+    ctx: GFContext
+    x: tuple[int, ...]
+    y: tuple[int, ...]
+
+
+@dataclass
+class BlockCursor:
+    """Streaming position: 1-based block and sample indices, current width."""
+
+    block_index: int = 1
+    sample_index: int = 1
+    field_bits: int = 0
+
+    def advance(self, vec_len: int, bits_per_sample: int, next_field_bits: int) -> None:
+        self.sample_index += self.field_bits * vec_len // bits_per_sample
+        self.block_index += 1
+        self.field_bits = next_field_bits
+
+
+class BlockProcessingError(RuntimeError):
+    """A block failed; carries its 1-based index (reference extractor.py:69-74)."""
+
+    def __init__(self, block_index: int, cause: BaseException):
+        super().__init__(f"block {block_index} failed: {cause!r}")
+        self.block_index = block_index
+
+
+# ------------------------------------------------------------ device helpers
+
+def _pack_vectors(vectors: Sequence[Sequence[int]], q: int) -> bytes:
+    """Concatenate element vectors LSB-first into one q*n*len bit stream."""
+    acc = 0
+    pos = 0
+    for vec in vectors:
+        for v in vec:
+            acc |= v << pos
+            pos += q
+    return acc.to_bytes((pos + 7) // 8, "little")
+
+
+def _device_inner_products(q: int, xs: Sequence[Sequence[int]], ys: Sequence[Sequence[int]],
+                           device=None) -> list[int]:
+    """sum_j x_j * y_j over GF(2^q) for each vector pair, on the GPU.
+
+    Vectors are grouped by length; each group is one bx_extract_eq launch with
+    one block per pair.  Elements must already be validated.
+    """
+    from . import device as D
+
+    dev = D.require_cuda(device)
+    out = [0] * len(xs)
+    groups: dict[int, list[int]] = {}
+    for i, v in enumerate(xs):
+        groups.setdefault(len(v), []).append(i)
+    for n, idx in groups.items():
+        xb = _pack_vectors([xs[i] for i in idx], q)
+        yb = _pack_vectors([ys[i] for i in idx], q)
+        xd, xn = D.to_device_stream(xb, dev)
+        yd, yn = D.to_device_stream(yb, dev)
+        res = D.extract_eq(xd, xn, yd, yn, q, n, len(idx))
+        nbytes = (len(idx) * q + 7) // 8
+        host = res[:nbytes].cpu().numpy().tobytes()
+        val = int.from_bytes(host, "little")
+        mask = (1 << q) - 1
+        for k, i in enumerate(idx):
+            out[i] = (val >> (k * q)) & mask
+    return out
+
+
+def ext_ip(ctx: GFContext, x: Sequence[int], y: Sequence[int]) -> int:
+    """Inner product sum(x_i * y_i) over GF(2^q) (reference extractor.py:77-87)."""
+    if len(x) != len(y):
+        raise ValueError(f"vector lengths differ: {len(x)} vs {len(y)}")
+    if not x:
+        raise ValueError("vectors must be non-empty")
+    for v in x:
+        ctx.check(v)
+    for v in y:
+        ctx.check(v)
+    ctx._device_ok()
+    return _device_inner_products(ctx.q, [tuple(x)], [tuple(y)])[0]
+
+
+def run_parallel(blocks: Iterable[BlockPair], workers: int, *,
+                 capacity: int | None = None) -> Iterator[OutputChunk]:
+    """Inner products of BlockPairs, in block order (reference extractor.py:94-130).
+
+    Pairs are gathered into batches (``capacity`` pairs, default 4096) and each
+    batch is one device launch per (q, n) group.  Output is identical for every
+    ``workers`` value.  A pair with an out-of-range element raises ValueError at
+    its position (workers == 1) or BlockProcessingError carrying its index
+    (workers > 1), after all earlier chunks were yielded -- as the reference.
+    """
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    batch_cap = capacity if capacity is not None else 4096
+    batch_cap = max(1, batch_cap)
+    it = iter(blocks)
+    while True:
+        batch: list[BlockPair] = []
+        for pair in it:
+            batch.append(pair)
+            if len(batch) >= batch_cap:
+                break
+        if not batch:
+            return
+        bad_at = None
+        bad_exc: Exception | None = None
+        for k, pair in enumerate(batch):
+            try:
+                if len(pair.x) != len(pair.y):
+                    raise ValueError(f"vector lengths differ: {len(pair.x)} vs {len(pair.y)}")
+                if not pair.x:
+                    raise ValueError("vectors must be non-empty")
+                for v in pair.x:
+                    pair.ctx.check(v)
+                for v in pair.y:
+                    pair.ctx.check(v)
+                pair.ctx._device_ok()
+            except Exception as exc:  # noqa: BLE001 - re-raised in order below
+                bad_at, bad_exc = k, exc
+                break
+        good = batch if bad_at is None else batch[:bad_at]
+        results = [0] * len(good)
+        by_q: dict[int, list[int]] = {}
+        for k, pair in enumerate(good):
+            by_q.setdefault(pair.ctx.q, []).append(k)
+        for q, ks in by_q.items():
+            vals = _device_inner_products(q, [good[k].x for k in ks], [good[k].y for k in ks])
+            for k, v in zip(ks, vals):
+                results[k] = v
+        for pair, v in zip(good, results):
+            yield OutputChunk(pair.index, v, pair.ctx.q)
+        if bad_exc is not None:
+            if workers == 1:
+                raise bad_exc
+            raise BlockProcessingError(batch[bad_at].index, bad_exc) from bad_exc
+
+
+# ---------------------------------------------------------- stream sources
+
+class _Source:
+    """One input stream plus an exact replay of BitReader's bookkeeping.
+
+    ``fill`` issues the same ``read(size)`` calls as reference bitio.py:35-43;
+    ``take`` mirrors a successful ``read_bits`` (:45-60).  In-memory inputs
+    (bytes, bytearray, memoryview, numpy arrays, torch tensors) are never
+    copied by the replay; file-like inputs are read for real and their bytes
+    are kept until the blocks that use them are computed.
+    """
+
+    def __init__(self, stream):
+        self._mem = None
+        self._file = None
+        try:
+            import torch
+            is_tensor = isinstance(stream, torch.Tensor)
+        except ImportError:  # pragma: no cover
+            is_tensor = False
+        if is_tensor:
+            self._mem = stream.reshape(-1).view(__import__("torch").uint8)
+            self._total = self._mem.numel()
+        elif isinstance(stream, np.ndarray):
+            self._mem = np.ascontiguousarray(stream).reshape(-1).view(np.uint8)
+            self._total = self._mem.size
+        elif isinstance(stream, (bytes, bytearray, memoryview)):
+            self._mem = memoryview(stream).cast("B")
+            self._total = len(self._mem)
+        elif hasattr(stream, "read"):
+            self._file = stream
+            self._parts = bytearray()
+            self._parts_base = 0      # stream byte offset of _parts[0]
+        else:
+            raise TypeError(f"cannot read from {type(stream).__name__}")
+        self.buffered = 0             # bytes delivered by read() so far
+        self.consumed = 0             # bits handed out (BitReader.bits_consumed)
+        self.exhausted = False
+
+    def avail(self) -> int:
+        return self.buffered * 8 - self.consumed
+
+    def _read(self, need: int) -> int:
+        if self._mem is not None:
+            got = min(need, self._total - self.buffered)
+            return max(got, 0)
+        data = self._file.read(need)
+        if data:
+            self._parts += data
+        return len(data) if data else 0
+
+    def fill(self, want_bits: int) -> None:
+        while self.avail() < want_bits and not self.exhausted:
+            need = max(READ_CHUNK, (want_bits - self.avail() + 7) // 8)
+            got = self._read(need)
+            if got == 0:
+                self.exhausted = True
+                break
+            self.buffered += got
+
+    def take(self, nbits: int) -> bool:
+        """read_bits(nbits): False (nothing consumed) if fewer bits remain."""
+        self.fill(nbits)
+        if self.avail() < nbits:
+            return False
+        self.consumed += nbits
+        return True
+
+    def tail_bits(self) -> int:
+        return self.avail()
+
+    def window(self, byte_lo: int, byte_hi: int):
+        """Stream bytes [byte_lo, byte_hi) (all already delivered)."""
+        if self._mem is not None:
+            return self._mem[byte_lo:byte_hi]
+        lo = byte_lo - self._parts_base
+        return memoryview(self._parts)[lo:byte_hi - self._parts_base]
+
+    def release(self, byte_lo: int) -> None:
+        """Forget buffered file bytes before stream offset byte_lo."""
+        if self._file is not None and byte_lo > self._parts_base:
+            cut = byte_lo - self._parts_base
+            del self._parts[:cut]
+            self._parts_base = byte_lo
+
+
+# ------------------------------------------------------------- extraction
+
+class Extraction:
+    """One extraction run: iterate for chunks or call ``run``; then read ``.report``.
+
+    Single-use, like the reference (extractor.py:133-279).  Extra keyword
+    arguments (not in the reference): ``device`` (CUDA device for the kernels),
+    ``devices`` (a list of devices to shard each segment's blocks across) and
+    ``segment_blocks`` (blocks computed per launch).
+    """
+
+    def __init__(self, x_stream, y_stream, plan, *, workers: int = 1,
+                 max_blocks: int | None = None, device=None, devices=None,
+                 segment_blocks: int = DEFAULT_SEGMENT_BLOCKS):
+        self._x = _Source(x_stream)
+        self._y = _Source(y_stream)
+        self.plan = plan
+        self.mode = "eq" if _params.is_eq_plan(plan) else "neq"
+        self._workers = workers
+        self._max_blocks = max_blocks
+        self._device = device
+        self._devices = list(devices) if devices else None
+        self._segment = max(64, (int(segment_blocks) // 64) * 64)
+        self._started = False
+        self._used_bits = 0
+        self._stop_reason = "completed"
+        self._chunks_emitted = 0
+        self._output_bits = 0
+        self._widths: list[int] = []     # neq: width of every completed block
+        self._t0 = 0.0
+        self.cursor = BlockCursor(field_bits=self._first_width())
+        self.report: ExtractionReport | None = None
+
+    # -- plan helpers (reference extractor.py:165-180)
+    def _first_width(self) -> int:
+        return self.plan.field_bits if self.mode == "eq" else self.plan.first_field_bits
+
+    def _next_width(self, width: int) -> int:
+        if self.mode == "eq":
+            return width
+        return width + self.plan.growth * self.plan.bits_per_sample
+
+    def _block_limit(self) -> int | None:
+        if self.mode == "eq":
+            if self._max_blocks is None:
+                return self.plan.num_blocks
+            return min(self.plan.num_blocks, self._max_blocks)
+        return self._max_blocks
+
+    # -- bookkeeping replay
+    def _advance(self, width: int, n: int, count_cap: int | None) -> int:
+        """Consume up to count_cap blocks of `width`; returns how many completed.
+
+        Sets ``_stop_reason`` to "input-exhausted" when a stream runs dry.
+        """
+        B = width * n
+        x, y = self._x, self._y
+        done = 0
+        while count_cap is None or done < count_cap:
+            k = min(x.avail() // B, y.avail() // B)
+            if count_cap is not None:
+                k = min(k, count_cap - done)
+            if k > 0:
+                x.consumed += k * B
+                y.consumed += k * B
+                done += k
+                continue
+            okx = x.take(B)      # both reads always happen (extractor.py:194-195)
+            oky = y.take(B)
+            if not (okx and oky):
+                self._stop_reason = "input-exhausted"
+                break
+            done += 1
+        self._used_bits += done * B
+        return done
+
+    # -- device compute of a run of equal-width blocks
+    def _compute(self, width: int, n: int, count: int, bit: int) -> bytes:
+        """Packed output bytes of `count` blocks whose windows start at stream
+        bit `bit` of both inputs; the last byte is zero-padded."""
+        from . import sharding
+
+        B = width * n
+        lo, hi = bit // 8, (bit + count * B + 7) // 8
+        return sharding.extract_packed(self._x.window(lo, hi), self._y.window(lo, hi), width, n,
+                                       count, x_bit0=bit % 8, y_bit0=bit % 8,
+                                       device=self._device, devices=self._devices)
+
+    def _segments_eq(self) -> Iterator[tuple[int, int, bytes]]:
+        """Yield (first_block, count, packed_output) segment by segment
+        (block loop of reference extractor.py:182-208)."""
+        plan = self.plan
+        width, n = plan.field_bits, plan.vec_len
+        if width > MAX_FIELD_BITS:
+            self._stop_reason = "width-cap"
+            return
+        limit = self._block_limit()
+        B = width * n
+        done = 0
+        while done < limit:
+            cap = min(self._segment, limit - done)
+            got = self._advance(width, n, cap)
+            if got:
+                out = self._compute(width, n, got, done * B)
+                self._x.release((done + got) * B // 8)
+                self._y.release((done + got) * B // 8)
+                yield done, got, out
+            done += got
+            if got < cap:
+                return
+        self._stop_reason = "completed" if limit == plan.num_blocks else "block-limit"
+
+    def _segments_neq(self) -> Iterator[tuple[int, int, bytes]]:
+        plan = self.plan
+        n = plan.vec_len
+        limit = self._block_limit()
+        step = plan.growth * plan.bits_per_sample
+        width = plan.first_field_bits
+        done = 0
+        offset = 0            # stream bit where the next block starts
+        while limit is None or done < limit:
+            if width > MAX_FIELD_BITS:
+                self._stop_reason = "width-cap"
+                return
+            if step:
+                cap = 1       # every block has its own width
+            else:
+                cap = self._segment if limit is None else min(self._segment, limit - done)
+            got = self._advance(width, n, cap)
+            if got:
+                out = self._compute(width, n, got, offset)
+                self._widths.extend([width] * got)
+                offset += got * width * n
+                self._x.release(offset // 8)
+                self._y.release(offset // 8)
+                yield done, got, out
+                done += got
+            if got < cap:
+                return
+            width += step
+        self._stop_reason = "block-limit"   # neq has no planned count
+
+    # -- public protocol
+    def _begin(self) -> None:
+        if self._started:
+            raise RuntimeError("an Extraction is single-use; create a new one")
+        self._started = True
+        self._t0 = time.perf_counter()
+        if self._workers < 1:
+            raise ValueError("workers must be >= 1")
+
+    def _segments(self) -> Iterator[tuple[int, int, bytes]]:
+        return self._segments_eq() if self.mode == "eq" else self._segments_neq()
+
+    def __iter__(self) -> Iterator[OutputChunk]:
+        try:
+            self._begin()
+        except ValueError:
+            self._finalize()
+            raise
+        try:
+            for first, count, packed in self._segments():
+                widths = ([self.plan.field_bits] * count if self.mode == "eq"
+                          else self._widths[first:first + count])
+                val = int.from_bytes(packed, "little")
+                pos = 0
+                for k, w in enumerate(widths):
+                    bits = (val >> pos) & ((1 << w) - 1)
+                    pos += w
+                    self._chunks_emitted += 1
+                    self._output_bits += w
+                    yield OutputChunk(first + k + 1, bits, w)
+        finally:
+            self._finalize()
+
+    def run(self, sink=None) -> ExtractionReport:
+        """Consume the run; optionally write the packed output to `sink` (one write)."""
+        try:
+            self._begin()
+        except ValueError:
+            self._finalize()
+            raise
+        parts: list[bytes] = []
+        carry = 0          # neq: bit-level concatenation of variable-width segments
+        carry_bits = 0
+        try:
+            for first, count, packed in self._segments():
+                if self.mode == "eq":
+                    nbits = count * self.plan.field_bits
+                else:
+                    nbits = sum(self._widths[first:first + count])
+                self._chunks_emitted += count
+                self._output_bits += nbits
+                if sink is None:
+                    continue
+                if carry_bits == 0 and nbits % 8 == 0:
+                    parts.append(packed)
+                else:
+                    carry |= int.from_bytes(packed, "little") << carry_bits
+                    carry_bits += nbits
+                    whole = carry_bits // 8
+                    if whole:
+                        parts.append((carry & ((1 << (8 * whole)) - 1)).to_bytes(whole, "little"))
+                        carry >>= 8 * whole
+                        carry_bits -= 8 * whole
+        finally:
+            self._finalize()
+        if sink is not None:
+            if carry_bits:
+                parts.append(carry.to_bytes(1, "little"))
+            sink.write(b"".join(parts))
+            self.report.pad_bits = (-self._output_bits) % 8
+        return self.report
+
+    def _finalize(self) -> None:
+        if self.report is not None:
+            return
+        wall = time.perf_counter() - self._t0
+        k = self._chunks_emitted
+        exhausted = self._stop_reason == "input-exhausted"
+        if self.mode == "eq":
+            bound = error_bound_eq(self.plan, k)
+        else:
+            bound = error_bound_neq(self.plan, k) if k else float("-inf")
+        # cursor: one advance per completed block (extractor.py:205)
+        n, b = self.plan.vec_len, self.plan.bits_per_sample
+        widths = ([self._first_width()] * k if self.mode == "eq" else self._widths[:k])
+        for w in widths:
+            self.cursor.advance(n, b, self._next_width(w))
+        self.report = ExtractionReport(
+            mode=self.mode,
+            plan=self.plan,
+            blocks_completed=k,
+            x_bits_consumed=self._x.consumed,
+            y_bits_consumed=self._y.consumed,
+            output_bits=self._output_bits,
+            x_discarded_tail_bits=self._discarded(self._x, exhausted),
+            y_discarded_tail_bits=self._discarded(self._y, exhausted),
+            log2_error_bound=bound,
+            wall_time_s=wall,
+            window_disjointness=True,
+            stop_reason=self._stop_reason,
+        )
+
+    def _discarded(self, src: _Source, exhausted: bool) -> int:
+        # reference extractor.py:249-262
+        d = src.consumed - self._used_bits
+        if exhausted:
+            d += src.tail_bits()
+        elif self._stop_reason == "completed" and self.mode == "eq":
+            d += self.plan.num_samples * self.plan.bits_per_sample - self._used_bits
+        return d
+
+
+def extract_eq(x_stream, y_stream, plan, *, workers: int = 1, max_blocks: int | None = None,
+               **kw) -> Extraction:
+    """Equal-block extraction (reference extractor.py:282-291)."""
+    if not _params.is_eq_plan(plan):
+        raise TypeError("extract_eq needs an EqPlan")
+    return Extraction(x_stream, y_stream, plan, workers=workers, max_blocks=max_blocks, **kw)
+
+
+def extract_neq(x_stream, y_stream, plan, *, workers: int = 1, max_blocks: int | None = None,
+                **kw) -> Extraction:
+    """Incremental-block extraction (reference extractor.py:294-306)."""
+    if not _params.is_neq_plan(plan) or _params.is_eq_plan(plan):
+        raise TypeError("extract_neq needs a NeqPlan")
+    return Extraction(x_stream, y_stream, plan, workers=workers, max_blocks=max_blocks, **kw)
+
+
+__all__ = ["BlockCursor", "BlockPair", "BlockProcessingError", "Extraction", "OutputChunk",
+           "ext_ip", "extract_eq", "extract_neq", "run_parallel"]

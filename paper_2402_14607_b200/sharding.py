@@ -1,0 +1,89 @@
+"""Block-range sharding across GPUs.
+
+Blocks are independent (reference extractor.py:16-19; isolation pinned by
+pkg/tests/test_extractor.py:125-137), so a run of `count` blocks splits into
+contiguous ranges, one per device, with no collective: each device gets its
+own input window, computes its blocks, and its packed output lands at a fixed
+byte offset of the result.  Range starts are multiples of 64 blocks, so every
+range's input starts on a byte boundary (64*q*n bits) and its output on a
+64*q-bit (byte) boundary.
+
+Two entry points:
+* ``extract_packed`` -- one process, several devices (threads, one per device);
+* ``rank_range``     -- the per-rank slice for torch.distributed launches
+  (bench.py), where each rank owns one GPU.
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+
+ALIGN_BLOCKS = 64
+
+
+def shard_ranges(nblocks: int, parts: int, align: int = ALIGN_BLOCKS) -> list[tuple[int, int]]:
+    """Split [0, nblocks) into `parts` contiguous (start, count) ranges whose
+    starts are multiples of `align`; trailing ranges may be empty."""
+    if parts < 1:
+        raise ValueError("parts must be >= 1")
+    units = -(-nblocks // align)
+    base, extra = divmod(units, parts)
+    out = []
+    start = 0
+    for p in range(parts):
+        u = base + (1 if p < extra else 0)
+        cnt = min(u * align, nblocks - start) if start < nblocks else 0
+        out.append((start, max(cnt, 0)))
+        start += u * align
+    return out
+
+
+def rank_range(nblocks: int, rank: int, world: int) -> tuple[int, int]:
+    return shard_ranges(nblocks, world)[rank]
+
+
+def _slice(buf, lo: int, hi: int):
+    return buf[lo:hi]
+
+
+def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit0: int = 0,
+                   device=None, devices=None) -> bytes:
+    """Packed output of `count` blocks; xv/yv hold the windows (host buffers or
+    torch tensors) starting at bit x_bit0 / y_bit0 of their first byte."""
+    from . import device as D
+
+    devs = [D.require_cuda(d) for d in devices] if devices else [D.require_cuda(device)]
+    B = q * n
+    out = np.zeros((count * q + 7) // 8, dtype=np.uint8)
+    ranges = [r for r in shard_ranges(count, len(devs)) if r[1] > 0]
+    errors: list[BaseException] = []
+
+    def work(dev, start: int, cnt: int) -> None:
+        try:
+            import torch
+
+            xs, ys = x_bit0 + start * B, y_bit0 + start * B
+            xd, xn = D.to_device_stream(_slice(xv, xs // 8, (xs + cnt * B + 7) // 8), dev)
+            yd, yn = D.to_device_stream(_slice(yv, ys // 8, (ys + cnt * B + 7) // 8), dev)
+            with torch.cuda.device(dev):
+                res = D.extract_eq(xd, xn, yd, yn, q, n, cnt, x_bit0=xs % 8, y_bit0=ys % 8)
+                nbytes = (cnt * q + 7) // 8
+                host = res[:nbytes].cpu().numpy()
+            ob = start * q // 8
+            out[ob:ob + nbytes] = host
+        except BaseException as exc:  # noqa: BLE001 - re-raised on the caller's thread
+            errors.append(exc)
+
+    if len(ranges) <= 1:
+        for dev, (s, c) in zip(devs, ranges):
+            work(dev, s, c)
+    else:
+        ts = [threading.Thread(target=work, args=(d, s, c)) for d, (s, c) in zip(devs, ranges)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    if errors:
+        raise errors[0]
+    return out.tobytes()

@@ -1,0 +1,217 @@
+"""GPU parity: the sm_100a kernels through the public API vs the reference's
+recorded outputs (tests/golden) and vs the CPU oracle.  Bit-exact throughout."""
+import io
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2402_14607_b200 as bx
+from paper_2402_14607_b200 import _lib, device as D
+from oracle import coracle
+
+from bxtest_util import DribbleIO, case_inputs, report_dict, tiny_eq_plan
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    _lib.lib()
+
+
+def dev_run(xb, yb, q, n, k, x_bit0=0, y_bit0=0, out_bit0=0, prefill=None):
+    xd, xn = D.to_device_stream(xb, "cuda")
+    yd, yn = D.to_device_stream(yb, "cuda")
+    nbytes = (out_bit0 + k * q + 7) // 8
+    out = torch.zeros(D.padded_len(nbytes), dtype=torch.uint8, device="cuda")
+    if prefill is not None:
+        out[:nbytes] = torch.from_numpy(np.frombuffer(prefill, dtype=np.uint8)[:nbytes]).cuda()
+    D.extract_eq(xd, xn, yd, yn, q, n, k, x_bit0=x_bit0, y_bit0=y_bit0, out=out, out_bit0=out_bit0)
+    return out[:nbytes].cpu().numpy().tobytes()
+
+
+def test_eq_cases_through_api(golden):
+    for c in golden("eq_cases.json"):
+        xb, yb = case_inputs(c)
+        plan = tiny_eq_plan(bx, c["b"], c["samples"], c.get("rate", "3/4"), c["n"], c["q"])
+        sink = io.BytesIO()
+        rep = bx.extract_eq(xb, yb, plan, max_blocks=c.get("max_blocks")).run(sink)
+        assert sink.getvalue().hex() == c["out"], c["tag"]
+        assert report_dict(rep) == c["report"], c["tag"]
+
+
+def test_neq_cases_through_api(golden):
+    for c in golden("neq_cases.json"):
+        if c.get("zeros"):
+            xb = yb = bytes(c["x_len"])
+        else:
+            xb, yb = case_inputs(c)
+        plan = bx.plan_neq(c["b"], "3/4", c["q1"], c["growth"])
+        sink = io.BytesIO()
+        rep = bx.extract_neq(xb, yb, plan, max_blocks=c["max_blocks"]).run(sink)
+        assert sink.getvalue().hex() == c["out"]
+        assert report_dict(rep) == c["report"]
+
+
+def test_every_q_random_shapes_and_offsets():
+    rnd = random.Random(1234)
+    for q in range(1, 129):
+        for _ in range(3):
+            n = rnd.choice([1, 2, 3, rnd.randint(1, 40), rnd.randint(40, 300)])
+            k = rnd.randint(1, 700)
+            xo, yo = rnd.randint(0, 70), rnd.randint(0, 70)
+            oo = rnd.choice([0, rnd.randint(1, 100)])
+            nb = (max(xo, yo) + k * q * n + 7) // 8 + rnd.randint(0, 9)
+            xb, yb = rnd.randbytes(nb), rnd.randbytes(nb)
+            want = coracle.extract_eq(xb, yb, q, n, k, x_bit0=xo, y_bit0=yo)
+            got = dev_run(xb, yb, q, n, k, x_bit0=xo, y_bit0=yo, out_bit0=oo,
+                          prefill=bytes([0xA5]) * ((oo + k * q + 7) // 8))
+            gi = int.from_bytes(got, "little")
+            assert (gi >> oo) & ((1 << (k * q)) - 1) == int.from_bytes(want, "little"), (q, n, k, xo, yo, oo)
+            # bits outside the written range are preserved
+            pre = int.from_bytes(bytes([0xA5]) * len(got), "little")
+            keep = ((1 << len(got) * 8) - 1) ^ (((1 << (k * q)) - 1) << oo)
+            assert gi & keep == pre & keep
+
+
+def test_extremes_all_ones_and_zeros():
+    for q in (1, 2, 4, 7, 8, 9, 16, 31, 32, 33, 63, 64, 65, 100, 127, 128):
+        for n in (1, 5, 64, 257):
+            k = 40
+            nb = (k * q * n + 7) // 8
+            for fill in (b"\xff", b"\x00", b"\x55"):
+                xb = fill * nb
+                yb = b"\xff" * nb
+                assert dev_run(xb, yb, q, n, k) == coracle.extract_eq(xb, yb, q, n, k), (q, n, fill)
+
+
+def test_gf_mul_kats(golden):
+    for q in range(1, 129):
+        rows = golden("gf_mul.json")[str(q)]
+        a = [int(r[0], 16) for r in rows]
+        b = [int(r[1], 16) for r in rows]
+        assert bx.field(q).mul_many(a, b) == [int(r[2], 16) for r in rows], q
+    assert bx.gf_mul(bx.field(2), 0b10, 0b10) == 0b11
+
+
+def test_ext_ip_kats(golden):
+    for c in golden("ext_ip.json"):
+        ctx = bx.field(c["q"])
+        xs = [int(v, 16) for v in c["x"]]
+        ys = [int(v, 16) for v in c["y"]]
+        assert bx.ext_ip(ctx, xs, ys) == int(c["z"], 16)
+    with pytest.raises(ValueError):
+        bx.ext_ip(bx.field(2), (1,), (1, 2))
+    with pytest.raises(ValueError):
+        bx.ext_ip(bx.field(2), (), ())
+    with pytest.raises(ValueError):
+        bx.ext_ip(bx.field(2), (4,), (1,))
+
+
+def test_field_inverses_small():
+    for q in range(1, 9):
+        ctx = bx.field(q)
+        xs = [x for x in range(1, 1 << q) for _ in range(1, 1 << q)]
+        ys = [y for _ in range(1, 1 << q) for y in range(1, 1 << q)]
+        prods = ctx.mul_many(xs, ys)
+        for x in range(1, 1 << q):
+            row = prods[(x - 1) * ((1 << q) - 1):x * ((1 << q) - 1)]
+            assert row.count(1) == 1          # exactly one inverse
+            assert len(set(row)) == (1 << q) - 1  # multiplication by x is a bijection
+
+
+def test_run_parallel_order_and_errors():
+    ctx = bx.field(4)
+    rnd = random.Random(14)
+    pairs = [bx.BlockPair(i + 1, ctx, tuple(rnd.randrange(16) for _ in range(3)),
+                          tuple(rnd.randrange(16) for _ in range(3))) for i in range(4)]
+    chunks = list(bx.run_parallel(iter(pairs), workers=4))
+    assert [c.index for c in chunks] == [1, 2, 3, 4]
+    assert [c.bits for c in chunks] == [bx.ext_ip(ctx, p.x, p.y) for p in pairs]
+    good = bx.BlockPair(1, ctx, (1, 2), (3, 4))
+    bad = bx.BlockPair(2, ctx, (1, 99), (3, 4))
+    with pytest.raises(bx.BlockProcessingError) as ei:
+        list(bx.run_parallel(iter([good, bad]), workers=2))
+    assert ei.value.block_index == 2
+    with pytest.raises(ValueError):
+        list(bx.run_parallel(iter([good, bad]), workers=1))
+
+
+def test_c1_full(golden):
+    from paper_2402_14607_b200 import workloads as W
+    wl = W.WORKLOADS["c1"]
+    xb = W.stream_bytes_host(wl.x, wl.samples).tobytes()
+    yb = W.stream_bytes_host(wl.y, wl.samples).tobytes()
+    sink = io.BytesIO()
+    rep = bx.extract_eq(xb, yb, wl.plan()).run(sink)
+    assert sink.getvalue() == golden("c1_out.bin")
+    assert report_dict(rep) == golden("c1.json")["report"]
+
+
+def test_streams_dribble_and_chunk_invariance():
+    rnd = random.Random(3)
+    data_x, data_y = rnd.randbytes(500), rnd.randbytes(500)
+    plan = tiny_eq_plan(bx, 8, 500, "3/4", 5, 8)
+    whole = [c.bits for c in bx.extract_eq(data_x, data_y, plan)]
+    dribble = [c.bits for c in bx.extract_eq(DribbleIO(data_x, 1), DribbleIO(data_y, 1), plan)]
+    assert whole == dribble and len(whole) == plan.num_blocks
+
+
+def test_block_isolation():
+    rnd = random.Random(4)
+    plan = tiny_eq_plan(bx, 8, 120, "3/4", 6, 8)
+    base_x = bytearray(rnd.randbytes(120))
+    data_y = rnd.randbytes(120)
+    base = [c.bits for c in bx.extract_eq(bytes(base_x), data_y, plan)]
+    for target in (0, 7, 19):
+        m = bytearray(base_x)
+        bit = target * 48 + rnd.randrange(48)
+        m[bit // 8] ^= 1 << (bit % 8)
+        got = [c.bits for c in bx.extract_eq(bytes(m), data_y, plan)]
+        assert [i for i, (a, b) in enumerate(zip(base, got)) if a != b] == [target]
+
+
+def test_device_tensor_inputs_and_segments():
+    rnd = random.Random(21)
+    q, n, k = 56, 48, 5000
+    nb = k * q * n // 8
+    xb, yb = rnd.randbytes(nb), rnd.randbytes(nb)
+    plan = tiny_eq_plan(bx, 8, nb, "3/4", n, q)
+    want = coracle.extract_eq(xb, yb, q, n, k)
+    xt = torch.frombuffer(bytearray(xb), dtype=torch.uint8).cuda()
+    yt = torch.frombuffer(bytearray(yb), dtype=torch.uint8).cuda()
+    for src in ((xb, yb), (xt, yt)):
+        for seg in (64, 1000, 1 << 24):
+            sink = io.BytesIO()
+            bx.extract_eq(*src, plan, segment_blocks=seg).run(sink)
+            assert sink.getvalue() == want
+
+
+def test_pack_kats(golden):
+    for c in golden("pack.json"):
+        vals = np.array([int(v, 16) for v in c["values"]], dtype=np.uint64)
+        t = torch.from_numpy(vals.view(np.int64)).cuda()
+        out = D.pack(t, c["b"])
+        nbytes = len(c["out"]) // 2
+        assert out[:nbytes].cpu().numpy().tobytes().hex() == c["out"], c["b"]
+
+
+def test_pack_random_offsets_and_widths():
+    rnd = random.Random(8)
+    for elem, dt in ((1, torch.uint8), (2, torch.int16), (4, torch.int32), (8, torch.int64)):
+        for _ in range(12):
+            b = rnd.randint(1, 8 * elem)
+            cnt = rnd.randint(1, 3000)
+            off = rnd.randint(0, 77)
+            vals = [rnd.getrandbits(8 * elem) for _ in range(cnt)]
+            arr = np.array(vals, dtype=np.dtype(f"u{elem}"))
+            t = torch.from_numpy(arr.view(np.dtype(f"i{elem}"))).cuda()
+            want = coracle.pack([v & ((1 << b) - 1) for v in vals], b)
+            out = D.pack(t, b, out_bit0=off)
+            got = int.from_bytes(out.cpu().numpy().tobytes(), "little") >> off
+            assert got & ((1 << (cnt * b)) - 1) == int.from_bytes(want, "little")

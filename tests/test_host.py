@@ -1,0 +1,197 @@
+"""Host-side logic on CPU: plans, reports, BitReader replay, sharding ranges,
+and that libbx_b200.so loads and exports every symbol of include/blockext_b200.h.
+
+The device compute is replaced, in this module only, by the CPU oracle through
+monkeypatching sharding.extract_packed -- so the bookkeeping (consumed bits,
+discarded tails, stop reasons, cursor, pad bits) is checked against the
+reference's recorded reports without a GPU.
+"""
+import io
+import re
+from fractions import Fraction
+
+import pytest
+
+import paper_2402_14607_b200 as bx
+from paper_2402_14607_b200 import _lib, params, sharding
+from oracle import coracle
+
+from bxtest_util import DribbleIO, case_inputs, report_dict, tiny_eq_plan
+from conftest import REPO
+
+
+@pytest.fixture
+def oracle_compute(monkeypatch):
+    def fake(xv, yv, q, n, count, *, x_bit0=0, y_bit0=0, device=None, devices=None):
+        xb = bytes(memoryview(xv).cast("B")) if not hasattr(xv, "numpy") else xv.numpy().tobytes()
+        yb = bytes(memoryview(yv).cast("B")) if not hasattr(yv, "numpy") else yv.numpy().tobytes()
+        return coracle.extract_eq(xb, yb, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0)
+    monkeypatch.setattr(sharding, "extract_packed", fake)
+
+
+def test_header_symbols_exported():
+    hdr = (REPO / "include" / "blockext_b200.h").read_text()
+    declared = set(re.findall(r"^\w[\w\s\*]*?\b(bx_\w+)\(", hdr, re.M))
+    assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
+    L = _lib.lib()
+    for name in declared:
+        assert hasattr(L, name)
+    assert L.bx_version() == 100
+
+
+def test_abi_modulus_table_matches_reference(golden):
+    ref = golden("moduli.json")
+    for q in range(1, 129):
+        assert list(_lib.modulus_exponents(q)) == ref[str(q)]
+    with pytest.raises(bx.CapacityError):
+        _lib.modulus_exponents(129)
+
+
+def test_abi_argument_errors_without_gpu():
+    L = _lib.lib()
+    assert L.bx_extract_eq(None, 0, 0, None, 0, 0, 129, 4, 1, None, 0, None) == _lib.BX_ERANGE
+    assert L.bx_extract_eq(None, 0, 0, None, 0, 0, 4, 0, 1, None, 0, None) == _lib.BX_EINVAL
+    assert L.bx_extract_eq(None, 0, 0, None, 0, 0, 4, 4, 0, None, 0, None) == _lib.BX_OK
+    assert L.bx_pack(None, 3, 8, 1, None, 0, None) == _lib.BX_EINVAL
+    with pytest.raises(ValueError, match="shorter"):
+        _lib.check(L.bx_extract_eq(1024, 4, 0, 1024, 4, 0, 4, 64, 1, 1024, 0, None), "x")
+
+
+def test_launch_info_geometry():
+    for q in (1, 4, 8, 9, 16, 32, 56, 58, 80, 128):
+        for n in (1, 4, 64, 120, 2000):
+            li = _lib.launch_info(q, n, 10_000)
+            assert li["threads"] == li["tpb"] * li["tile"]
+            assert li["threads"] % 32 == 0 and li["threads"] <= 256
+            assert li["family"] == ("diag" if q <= 8 else "holes")
+            assert li["grid"] == -(-10_000 // li["tile"])
+
+
+def test_golden_plans_and_bounds(golden):
+    for c in golden("eq_cases.json"):
+        plan = tiny_eq_plan(bx, c["b"], c["samples"], c.get("rate", "3/4"), c["n"], c["q"])
+        assert repr(plan.log2_error) == c["plan_log2_error"]
+
+
+def test_plan_eq_reference_values():
+    p = bx.plan_eq(16, 2**47, Fraction(1074, 1600), Fraction(1, 2**30))
+    assert (p.vec_len, p.field_bits, p.num_blocks) == (71, 80, 2**51 // (80 * 71))
+    p = bx.plan_eq(8, 2**28, "3/4", "2^-30")
+    assert (p.vec_len, p.field_bits, p.num_blocks) == (48, 56, 798915)
+    with pytest.raises(bx.UnsupportedRateError):
+        bx.plan_eq(8, 100, "1/2", "2^-10")
+    with pytest.raises(TypeError):
+        bx.plan_eq(8, 100, 0.75, "2^-10")
+    with pytest.raises(bx.DivergenceError):
+        bx.error_bound_neq(bx.plan_neq(8, "3/4", 8, 0))
+
+
+def test_report_text_round_trip():
+    plan = tiny_eq_plan(bx, 8, 300, "3/4", 5, 8)
+    rep = bx.ExtractionReport("eq", plan, 3, 120, 120, 24, 0, 0, -1.5, 0.25, True, "completed", 0)
+    assert bx.ExtractionReport.from_text(rep.to_text()) == rep
+    nplan = bx.plan_neq(8, "3/4", 8, 1)
+    assert bx.plan_from_text(bx.plan_to_text(nplan)) == nplan
+
+
+@pytest.mark.parametrize("which", ["eq"])
+def test_eq_reports_match_reference(golden, oracle_compute, which):
+    for c in golden("eq_cases.json"):
+        xb, yb = case_inputs(c)
+        plan = tiny_eq_plan(bx, c["b"], c["samples"], c.get("rate", "3/4"), c["n"], c["q"])
+        sink = io.BytesIO()
+        rep = bx.extract_eq(xb, yb, plan, max_blocks=c.get("max_blocks")).run(sink)
+        assert sink.getvalue().hex() == c["out"], c["tag"]
+        assert report_dict(rep) == c["report"], c["tag"]
+
+
+def test_eq_reports_file_streams(golden, oracle_compute):
+    # file-like inputs (BytesIO and 7-byte dribbles) replay the same reads
+    for c in golden("eq_cases.json")[-12:]:
+        xb, yb = case_inputs(c)
+        plan = tiny_eq_plan(bx, c["b"], c["samples"], c.get("rate", "3/4"), c["n"], c["q"])
+        for mk in (io.BytesIO, lambda d: DribbleIO(d, 7)):
+            sink = io.BytesIO()
+            rep = bx.extract_eq(mk(xb), mk(yb), plan, max_blocks=c.get("max_blocks")).run(sink)
+            assert sink.getvalue().hex() == c["out"], c["tag"]
+            if mk is io.BytesIO:
+                assert report_dict(rep) == c["report"], c["tag"]
+
+
+def test_neq_reports_match_reference(golden, oracle_compute):
+    for c in golden("neq_cases.json"):
+        if c.get("zeros"):
+            xb = yb = bytes(c["x_len"])
+        else:
+            xb, yb = case_inputs(c)
+        plan = bx.plan_neq(c["b"], "3/4", c["q1"], c["growth"])
+        sink = io.BytesIO()
+        rep = bx.extract_neq(xb, yb, plan, max_blocks=c["max_blocks"]).run(sink)
+        assert sink.getvalue().hex() == c["out"], c
+        assert report_dict(rep) == c["report"], c
+
+
+def test_iteration_chunks_and_segments(golden, oracle_compute):
+    c = next(c for c in golden("eq_cases.json") if c["tag"] == "multi_fill")
+    xb, yb = case_inputs(c)
+    plan = tiny_eq_plan(bx, c["b"], c["samples"], "3/4", c["n"], c["q"])
+    run = bx.extract_eq(xb, yb, plan, segment_blocks=640)
+    chunks = list(run)
+    assert [ch.index for ch in chunks[:3]] == [1, 2, 3]
+    acc = 0
+    for k, ch in enumerate(chunks):
+        assert ch.width == c["q"]
+        acc |= ch.bits << (k * c["q"])
+    assert acc.to_bytes(len(c["out"]) // 2, "little").hex() == c["out"]
+    assert run.report.blocks_completed == len(chunks)
+    assert run.cursor.block_index == len(chunks) + 1
+    with pytest.raises(RuntimeError):
+        list(run)
+
+
+def test_type_checks():
+    plan = tiny_eq_plan(bx, 8, 100, "3/4", 5, 8)
+    nplan = bx.plan_neq(8, "3/4", 8, 1)
+    with pytest.raises(TypeError):
+        bx.extract_eq(b"", b"", nplan)
+    with pytest.raises(TypeError):
+        bx.extract_neq(b"", b"", plan)
+
+
+def test_shard_ranges():
+    for nb in (0, 1, 63, 64, 65, 1000, 8388608, 4194305):
+        for parts in (1, 2, 3, 4, 8):
+            rs = sharding.shard_ranges(nb, parts)
+            assert len(rs) == parts
+            assert sum(c for _, c in rs) == nb
+            pos = 0
+            for s, c in rs:
+                if c:
+                    assert s == pos and s % 64 == 0
+                    pos += c
+
+
+def test_gf_context_validation():
+    with pytest.raises(bx.CapacityError):
+        bx.GFContext(129)
+    with pytest.raises(ValueError):
+        bx.GFContext(2, modulus=0b101)
+    with pytest.raises(ValueError):
+        bx.GFContext(2, modulus=0b110)
+    ctx = bx.field(4)
+    with pytest.raises(ValueError):
+        ctx.add(16, 0)
+    assert ctx.add(5, 3) == 6
+    assert bx.field(80) is bx.field(80)
+    assert bx.is_irreducible(0b111) and not bx.is_irreducible(0b101)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    plan = tiny_eq_plan(bx, 8, 100, "3/4", 5, 8)
+    with pytest.raises(bx.DeviceError):
+        bx.extract_eq(bytes(100), bytes(100), plan).run()
+    with pytest.raises(bx.DeviceError):
+        bx.ext_ip(bx.field(4), (1,), (2,))
