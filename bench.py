@@ -222,15 +222,13 @@ def run_ours(args, wl) -> None:
     xs = dataclasses.replace(wl.x, seed=wl.x.seed + 1000 * rank)
     ys = dataclasses.replace(wl.y, seed=wl.y.seed + 1000 * rank)
     t_gen = time.perf_counter()
-    xh = W.stream_bytes_host(xs, wl.samples)
-    yh = W.stream_bytes_host(ys, wl.samples)
+    xd, nbytes = W.stream_device(xs, wl.samples, dev)
+    yd, _ = W.stream_device(ys, wl.samples, dev)
+    xh = xd[:nbytes].cpu().numpy()
+    yh = yd[:nbytes].cpu().numpy()
     t_gen = time.perf_counter() - t_gen
-    nbytes = wl.stream_bytes
     B = wl.block_bits
     nblocks = wl.num_blocks
-
-    xd, _ = D.to_device_stream(xh, dev)
-    yd, _ = D.to_device_stream(yh, dev)
     obytes = (nblocks * wl.q + 7) // 8
     out = torch.zeros(D.padded_len(obytes), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)

@@ -65,7 +65,8 @@ int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0,
  * Launch geometry bx_extract_eq would use (for tests, benches and profiling):
  * threads per block-pair group, blocks per CTA tile, staged (1) or direct (0),
  * CTA threads, dynamic shared memory bytes, grid size, and kernel family
- * (0 = diag, 1 = holes).  Any output pointer may be NULL.
+ * (bit 0: 0 = diag, 1 = holes; bit 1 set = aligned direct kernel), for
+ * 16-byte aligned buffers starting at bit 0.  Any output pointer may be NULL.
  */
 int bx_launch_info(int q, int n, int64_t nblocks, int* tpb, int* tile, int* staged,
                    int* threads, int* smem_bytes, int64_t* grid, int* family);

@@ -81,7 +81,7 @@ def launch_info(q: int, n: int, nblocks: int) -> dict:
     tpb, tile, staged, threads, smem = (v.value for v in vals[:5])
     return {"tpb": tpb, "tile": tile, "staged": staged, "threads": threads,
             "smem_bytes": smem, "grid": grid.value,
-            "family": "diag" if fam.value == 0 else "holes"}
+            "family": ("diag", "holes")[fam.value & 1], "direct": bool(fam.value & 2)}
 
 
 def launch_count(reset: bool = False) -> int:

@@ -59,14 +59,17 @@ int bx_launch_info(int q, int n, int64_t nblocks, int* tpb, int* tile, int* stag
                    int* threads, int* smem_bytes, int64_t* grid, int* family) {
   if (q < 1 || q > 128) return fail(BX_ERANGE, "field width outside 1..128");
   if (n < 1 || nblocks < 0) return fail(BX_EINVAL, "n must be >= 1 and nblocks >= 0");
-  const bx::LaunchCfg c = bx::choose_launch(q, n, nblocks);
+  // geometry for 16-byte aligned buffers starting at bit 0
+  const void* al = reinterpret_cast<const void*>(uintptr_t(256));
+  const bx::LaunchCfg c = bx::direct_ok(q, n, 0, 0, 0, al, al) ? bx::choose_direct(q, n, nblocks)
+                                                               : bx::choose_launch(q, n, nblocks);
   if (tpb) *tpb = 1 << c.tpb_log2;
   if (tile) *tile = c.tile;
   if (staged) *staged = c.staged;
   if (threads) *threads = c.threads;
   if (smem_bytes) *smem_bytes = (int)c.smem;
   if (grid) *grid = c.grid;
-  if (family) *family = c.family;
+  if (family) *family = c.family + (c.direct ? 2 : 0);
   return BX_OK;
 }
 
@@ -86,7 +89,9 @@ int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0, const void* y,
     return fail(BX_EINVAL, "block range overflows");
   if (x_bit0 + nblocks * B > 8 * x_bytes) return fail(BX_EINVAL, "x stream shorter than the block range");
   if (y_bit0 + nblocks * B > 8 * y_bytes) return fail(BX_EINVAL, "y stream shorter than the block range");
-  const bx::LaunchCfg c = bx::choose_launch(q, n, nblocks);
+  const bx::LaunchCfg c = bx::direct_ok(q, n, x_bit0, y_bit0, out_bit0, x, y)
+                              ? bx::choose_direct(q, n, nblocks)
+                              : bx::choose_launch(q, n, nblocks);
   if (c.grid > 0x7FFFFFFF) return fail(BX_EINVAL, "too many blocks for one launch");
   bx::EqArgs a;
   a.x = static_cast<const uint32_t*>(x);

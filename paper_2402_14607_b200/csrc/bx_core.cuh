@@ -179,17 +179,22 @@ struct Diag {
     return m;
   }
 
-  // unreduced c (2Q-1 <= 15 bits)
+  // unreduced c (2Q-1 <= 15 bits): c_k = parity(XOR_b acc_{k-2b} & M_b), one
+  // LOP3 per (k, b) pair and one POPC per k.
   __device__ __forceinline__ uint32_t unreduced() const {
     uint32_t c = 0;
 #pragma unroll
-    for (int b = 0; b < Q; b++) {
+    for (int k = 0; k < 2 * Q - 1; k++) {
+      uint32_t t = 0;
 #pragma unroll
-      for (int a = 0; a < Q; a++) {
+      for (int b = 0; b < Q; b++) {
+        const int a = k - b;
+        if (a < 0 || a >= Q) continue;
         const int d = a - b;
         const uint32_t acc = d >= 0 ? pos[d] : neg[-d];
-        c ^= (uint32_t)(__popc(acc & mask_b(b)) & 1) << (a + b);
+        t ^= acc & mask_b(b);
       }
+      c |= (uint32_t)(__popc(t) & 1) << k;
     }
     return c;
   }
@@ -381,6 +386,111 @@ __global__ void __launch_bounds__(256) eq_kernel(const EqArgs a) {
       const uint32_t mask = (nbits >= 32 ? 0xFFFFFFFFu : ((1u << nbits) - 1u)) << off;
       atomicAnd(&a.out[gw0 + i], ~mask);
       atomicOr(&a.out[gw0 + i], v & mask);
+    }
+  }
+}
+
+
+// ------------------------------------------------------- direct kernel
+//
+// Aligned fast path: Q in {1,2,4,8,16,32,64,128}, q*n a multiple of 128 bits,
+// 16-byte aligned stream starts, word-aligned output.  One thread per block;
+// the block's windows are read with 128-bit loads straight from HBM (each
+// 128-bit unit holds 128/Q whole elements), no shared-memory staging.  The
+// outputs of a warp's 32 consecutive blocks are OR-combined with shuffles
+// into whole 32-bit words (Q < 32) or stored directly (Q >= 32).
+struct DirectArgs {
+  const uint4* x;      // 16-byte aligned start of block 0's window
+  const uint4* y;
+  int64_t nblocks;
+  uint32_t* out;       // word holding output bit 0 of block 0
+  int units;           // 128-bit units per block (q*n/128)
+};
+
+template <int Q>
+__device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void* accp) {
+  if constexpr (Q <= kDiagMaxQ) {
+    Diag<Q>& acc = *static_cast<Diag<Q>*>(accp);
+    acc.add(X.x, Y.x);
+    acc.add(X.y, Y.y);
+    acc.add(X.z, Y.z);
+    acc.add(X.w, Y.w);
+  } else {
+    Holes<Q>& acc = *static_cast<Holes<Q>*>(accp);
+    constexpr int EW = cdiv(Q, 32);
+    const uint32_t xs[4] = {X.x, X.y, X.z, X.w};
+    const uint32_t ys[4] = {Y.x, Y.y, Y.z, Y.w};
+    if constexpr (Q == 16) {
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        uint32_t a0[1] = {xs[i] & 0xFFFFu}, b0[1] = {ys[i] & 0xFFFFu};
+        uint32_t a1[1] = {xs[i] >> 16}, b1[1] = {ys[i] >> 16};
+        acc.add(a0, b0);
+        acc.add(a1, b1);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4 / EW; e++) {
+        uint32_t a[EW], b[EW];
+#pragma unroll
+        for (int i = 0; i < EW; i++) {
+          a[i] = xs[e * EW + i];
+          b[i] = ys[e * EW + i];
+        }
+        acc.add(a, b);
+      }
+    }
+  }
+}
+
+template <int Q>
+__global__ void __launch_bounds__(256) eq_direct_kernel(const DirectArgs a) {
+  constexpr int EW = cdiv(Q, 32);
+  constexpr int CW = cdiv(2 * Q - 1, 32);
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  Wide<EW> z = wzero<EW>();
+  if (l < a.nblocks) {
+    const uint4* xp = a.x + l * a.units;
+    const uint4* yp = a.y + l * a.units;
+    Wide<CW> c;
+    if constexpr (Q <= kDiagMaxQ) {
+      Diag<Q> acc;
+      acc.init();
+#pragma unroll 4
+      for (int u = 0; u < a.units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+      c.w[0] = acc.unreduced();
+    } else {
+      Holes<Q> acc;
+      acc.init();
+#pragma unroll 2
+      for (int u = 0; u < a.units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+      c = acc.unreduced();
+    }
+    z = reduce<Q>(c);
+  }
+  if constexpr (Q < 32) {
+    // 32/Q consecutive blocks share one output word
+    constexpr int G = 32 / Q;
+    uint32_t v = z.w[0] << ((lane % G) * Q);
+#pragma unroll
+    for (int m = 1; m < G; m <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, m);
+    const int64_t first = l - (lane % G);      // first block of this word
+    if ((lane % G) == 0 && first < a.nblocks) {
+      const int64_t w = first * Q / 32;
+      const int64_t valid = (a.nblocks - first) * Q;
+      if (valid >= 32) {
+        a.out[w] = v;
+      } else {
+        const uint32_t mask = (1u << valid) - 1u;
+        atomicAnd(&a.out[w], ~mask);
+        atomicOr(&a.out[w], v & mask);
+      }
+    }
+  } else {
+    if (l < a.nblocks) {
+#pragma unroll
+      for (int i = 0; i < EW; i++) a.out[l * EW + i] = z.w[i];
     }
   }
 }

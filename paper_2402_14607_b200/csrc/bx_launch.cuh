@@ -17,7 +17,21 @@ struct LaunchCfg {
   size_t smem = 0;
   int64_t grid = 0;
   int family = 0;     // 0 diag, 1 holes
+  int direct = 0;     // 1: eq_direct_kernel (aligned fast path)
+  int units = 0;      // direct: 128-bit units per block
 };
+
+inline bool direct_q(int q) {
+  return q == 1 || q == 2 || q == 4 || q == 8 || q == 16 || q == 32 || q == 64 || q == 128;
+}
+
+// Aligned fast path eligibility (see eq_direct_kernel).
+inline bool direct_ok(int q, int n, int64_t x_bit0, int64_t y_bit0, int64_t out_bit0,
+                      const void* x, const void* y) {
+  const int64_t B = (int64_t)q * n;
+  return direct_q(q) && B % 128 == 0 && x_bit0 % 128 == 0 && y_bit0 % 128 == 0 &&
+         out_bit0 % 32 == 0 && (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
+}
 
 constexpr size_t kStageBudget = 96 * 1024;    // preferred smem per CTA
 constexpr size_t kStageMax = 200 * 1024;      // hard cap before going direct
@@ -59,8 +73,34 @@ inline LaunchCfg choose_launch(int q, int n, int64_t nblocks) {
   return c;
 }
 
+inline LaunchCfg choose_direct(int q, int n, int64_t nblocks) {
+  LaunchCfg c;
+  c.family = q <= kDiagMaxQ ? 0 : 1;
+  c.direct = 1;
+  c.tpb_log2 = 0;
+  c.tile = 256;
+  c.threads = 256;
+  c.staged = 0;
+  c.smem = 0;
+  c.units = (int)((int64_t)q * n / 128);
+  c.grid = (nblocks + 255) / 256;
+  return c;
+}
+
 template <int Q>
 cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
+  if constexpr (Q == 1 || Q == 2 || Q == 4 || Q == 8 || Q == 16 || Q == 32 || Q == 64 || Q == 128) {
+    if (c.direct) {
+      DirectArgs d;
+      d.x = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a.x) + a.x_bit0 / 8);
+      d.y = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a.y) + a.y_bit0 / 8);
+      d.nblocks = a.nblocks;
+      d.out = a.out + a.out_bit0 / 32;
+      d.units = c.units;
+      eq_direct_kernel<Q><<<(unsigned)c.grid, c.threads, 0, s>>>(d);
+      return cudaGetLastError();
+    }
+  }
   if (c.staged) {
     auto k = eq_kernel<Q, true>;
     if (c.smem > 48 * 1024) {

@@ -499,9 +499,13 @@ class Extraction:
             bound = error_bound_neq(self.plan, k) if k else float("-inf")
         # cursor: one advance per completed block (extractor.py:205)
         n, b = self.plan.vec_len, self.plan.bits_per_sample
-        widths = ([self._first_width()] * k if self.mode == "eq" else self._widths[:k])
-        for w in widths:
-            self.cursor.advance(n, b, self._next_width(w))
+        if self.mode == "eq" or self.plan.growth == 0:
+            w = self._first_width()       # constant width: closed form of k advances
+            self.cursor.sample_index += k * (w * n // b)
+            self.cursor.block_index += k
+        else:
+            for w in self._widths[:k]:
+                self.cursor.advance(n, b, self._next_width(w))
         self.report = ExtractionReport(
             mode=self.mode,
             plan=self.plan,

@@ -238,3 +238,27 @@ def _block_markov_host(spec: SourceSpec, samples: int) -> np.ndarray:
         prev = chain[-1].copy()
         k += c
     return out.view(np.uint8)
+
+
+# ---------------------------------------------------------------- device RNG
+
+def to_model(spec: SourceSpec):
+    from . import sources as S
+
+    if spec.kind == "iid-biased":
+        return S.iid_biased(spec.p, seed=spec.seed)
+    if spec.kind == "iid-table":
+        return S.iid_table(spec.pmf(), spec.bits_per_sample, seed=spec.seed)
+    raise ValueError(f"no reference model for {spec.kind}")
+
+
+def stream_device(spec: SourceSpec, samples: int, device=None):
+    """(padded device buffer, nbytes) of the stream; host PCG64 draws, device
+    mapping and packing (byte-identical to ``stream_bytes_host``)."""
+    from . import device as D
+    from . import sources as S
+
+    if spec.kind == "block-markov":
+        host = _block_markov_host(spec, samples)
+        return D.to_device_stream(host, D.require_cuda(device))
+    return S.generate_device(to_model(spec), samples, device)

@@ -64,6 +64,7 @@ def test_launch_info_geometry():
             assert li["threads"] == li["tpb"] * li["tile"]
             assert li["threads"] % 32 == 0 and li["threads"] <= 256
             assert li["family"] == ("diag" if q <= 8 else "holes")
+            assert li["direct"] == (q in (1, 2, 4, 8, 16, 32, 64, 128) and q * n % 128 == 0)
             assert li["grid"] == -(-10_000 // li["tile"])
 
 
