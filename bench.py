@@ -287,8 +287,10 @@ def run_ours(args, wl) -> None:
                 "frac": achieved / peak, "traffic": _traffic(wl.name),
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes,
-                "kernel_ms": ms_step, "kernel": f"bx::eq_kernel<{wl.q}, staged>",
-                "launch": _lib.launch_info(wl.q, wl.n, nblocks)}
+                "kernel_ms": ms_step, "launch": _lib.launch_info(wl.q, wl.n, nblocks)}
+    li = roofline["launch"]
+    roofline["kernel"] = (f"bx::eq_direct_kernel<{wl.q}, {wl.block_bits // 128}>" if li["direct"]
+                          else f"bx::eq_kernel<{wl.q}, {'true' if li['staged'] else 'false'}>")
 
     # ---- e2e: public API from pinned host memory, every step H2D + D2H
     xp = torch.from_numpy(xh).pin_memory()

@@ -158,8 +158,12 @@ template <int Q>
 struct Diag {
   static constexpr int E = 32 / Q;   // elements per 32-bit chunk
   static constexpr int EB = E * Q;   // bits per chunk
-  uint32_t pos[Q];                   // d = 0 .. Q-1
-  uint32_t neg[Q];                   // d = -1 .. -(Q-1) at index 1 .. Q-1
+  // pos[d] (d >= 0) accumulates X & (Y << d): bit jQ+b+d holds x_{j,b+d} y_{j,b}.
+  // neg[d] (d >= 1) accumulates (X << d) & Y: bit jQ+b holds x_{j,b-d} y_{j,b}.
+  // Only left shifts, so the compiler issues them as IMAD.SHL on the FMA pipe
+  // and the ALU pipe carries just the 2Q-1 LOP3s per chunk.
+  uint32_t pos[Q];
+  uint32_t neg[Q];
 
   __device__ __forceinline__ void init() {
 #pragma unroll
@@ -168,7 +172,7 @@ struct Diag {
 
   __device__ __forceinline__ void add(uint32_t X, uint32_t Y) {
 #pragma unroll
-    for (int d = 0; d < Q; d++) pos[d] ^= (X >> d) & Y;
+    for (int d = 0; d < Q; d++) pos[d] ^= X & (Y << d);
 #pragma unroll
     for (int d = 1; d < Q; d++) neg[d] ^= (X << d) & Y;
   }
@@ -180,7 +184,8 @@ struct Diag {
   }
 
   // unreduced c (2Q-1 <= 15 bits): c_k = parity(XOR_b acc_{k-2b} & M_b), one
-  // LOP3 per (k, b) pair and one POPC per k.
+  // LOP3 per (k, b) pair and one POPC per k.  For d >= 0 the product
+  // x_{j,a} y_{j,b} (a = b + d) sits at bit jQ+a of pos[d], i.e. under M_a.
   __device__ __forceinline__ uint32_t unreduced() const {
     uint32_t c = 0;
 #pragma unroll
@@ -191,8 +196,8 @@ struct Diag {
         const int a = k - b;
         if (a < 0 || a >= Q) continue;
         const int d = a - b;
-        const uint32_t acc = d >= 0 ? pos[d] : neg[-d];
-        t ^= acc & mask_b(b);
+        if (d >= 0) t ^= pos[d] & mask_b(a);
+        else t ^= neg[-d] & mask_b(b);
       }
       c |= (uint32_t)(__popc(t) & 1) << k;
     }
@@ -443,7 +448,7 @@ __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void
   }
 }
 
-template <int Q>
+template <int Q, int U>
 __global__ void __launch_bounds__(256) eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
@@ -454,17 +459,20 @@ __global__ void __launch_bounds__(256) eq_direct_kernel(const DirectArgs a) {
     const uint4* xp = a.x + l * a.units;
     const uint4* yp = a.y + l * a.units;
     Wide<CW> c;
+    // U > 0: the unit count is a compile-time constant (fully unrolled,
+    // all loads issued up front); U == 0: runtime count.
+    const int units = U > 0 ? U : a.units;
     if constexpr (Q <= kDiagMaxQ) {
       Diag<Q> acc;
       acc.init();
 #pragma unroll 4
-      for (int u = 0; u < a.units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+      for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
       c.w[0] = acc.unreduced();
     } else {
       Holes<Q> acc;
       acc.init();
 #pragma unroll 2
-      for (int u = 0; u < a.units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+      for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
       c = acc.unreduced();
     }
     z = reduce<Q>(c);

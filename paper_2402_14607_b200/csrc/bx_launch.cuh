@@ -97,7 +97,14 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
       d.nblocks = a.nblocks;
       d.out = a.out + a.out_bit0 / 32;
       d.units = c.units;
-      eq_direct_kernel<Q><<<(unsigned)c.grid, c.threads, 0, s>>>(d);
+      const dim3 g((unsigned)c.grid), b(c.threads);
+      switch (c.units) {
+        case 1: eq_direct_kernel<Q, 1><<<g, b, 0, s>>>(d); break;
+        case 2: eq_direct_kernel<Q, 2><<<g, b, 0, s>>>(d); break;
+        case 4: eq_direct_kernel<Q, 4><<<g, b, 0, s>>>(d); break;
+        case 8: eq_direct_kernel<Q, 8><<<g, b, 0, s>>>(d); break;
+        default: eq_direct_kernel<Q, 0><<<g, b, 0, s>>>(d); break;
+      }
       return cudaGetLastError();
     }
   }
