@@ -26,7 +26,9 @@
 //    coefficients sit at positions = (i+k) mod 3 and each coefficient count is
 //    <= 6 < 8, so no carry reaches the next same-residue position: bit p of the
 //    product is the parity of the count, i.e. the carry-less coefficient.
-//    Products are XOR-accumulated per (slot, residue) and masked once per block.
+//    Halves are combined with Karatsuba (K(8) = 27 half products for q=128
+//    instead of 64); leaf products are XOR-accumulated per residue over the
+//    whole block and recombined and masked once per block.
 //    IMAD.WIDE is avoided: it issues at 1/3 the rate of IMAD on sm_100a
 //    (profiles/r01_pipes_microbench.txt).
 //
@@ -207,60 +209,106 @@ struct Diag {
 
 // ---------------------------------------------------------- holes (Q >= 9)
 
+// One 16x16 carry-less half product with nine 32-bit IMADs on holed operands,
+// XOR-accumulated per residue class (see the header comment).
+__device__ __forceinline__ void holes16(uint32_t xh, uint32_t yh, uint32_t (&acc)[3]) {
+  const uint32_t x0 = xh & 0x9249u, x1 = xh & 0x2492u, x2 = xh & 0x4924u;
+  const uint32_t y0 = yh & 0x9249u, y1 = yh & 0x2492u, y2 = yh & 0x4924u;
+  acc[0] ^= (x0 * y0) ^ (x1 * y2) ^ (x2 * y1);
+  acc[1] ^= (x0 * y1) ^ (x1 * y0) ^ (x2 * y2);
+  acc[2] ^= (x0 * y2) ^ (x1 * y1) ^ (x2 * y0);
+}
+
+// Karatsuba over 16-bit halves.  A size-M operand pair splits into
+// L = x_L*y_L, H = x_H*y_H and Mid = (x_L+x_H)(y_L+y_H); in GF(2)[t]
+//     x*y = L (1 + t^h) + Mid t^h + H (t^h + t^2h),   t = x^16, h = ceil(M/2).
+// Leaves are single half products; they are accumulated over the whole block
+// (all j) and recombined once per block -- the sum over j commutes with the
+// linear recombination, so Karatsuba's extra additions are paid per block,
+// not per element.  Leaves per size: K(1)=1, K(m)=2K(ceil(m/2))+K(floor(m/2))
+// (K(2)=3, K(4)=9, K(8)=27 vs 4, 16, 64 half products for schoolbook).
+__host__ __device__ constexpr int kara_leaves(int m) {
+  return m <= 1 ? 1 : 2 * kara_leaves((m + 1) / 2) + kara_leaves(m / 2);
+}
+
+template <int M, int L0, int K>
+__device__ __forceinline__ void kara_acc(const uint32_t* xo, const uint32_t* yo,
+                                         uint32_t (&acc)[K][3]) {
+  if constexpr (M == 1) {
+    holes16(xo[0], yo[0], acc[L0]);
+  } else {
+    constexpr int h = (M + 1) / 2;
+    kara_acc<h, L0, K>(xo, yo, acc);
+    kara_acc<M - h, L0 + kara_leaves(h), K>(xo + h, yo + h, acc);
+    uint32_t xm[h], ym[h];
+#pragma unroll
+    for (int i = 0; i < h; i++) {
+      xm[i] = (i + h < M) ? (xo[i] ^ xo[i + h]) : xo[i];
+      ym[i] = (i + h < M) ? (yo[i] ^ yo[i + h]) : yo[i];
+    }
+    kara_acc<h, L0 + kara_leaves(h) + kara_leaves(M - h), K>(xm, ym, acc);
+  }
+}
+
+template <int CW>
+__device__ __forceinline__ void placed_xor(Wide<CW>& c, uint32_t cs, int s) {
+  // c ^= cs << (16*s); s is a compile-time constant after unrolling
+  const int w = (16 * s) >> 5;
+  if ((s & 1) == 0) {
+    if (w < CW) c.w[w] ^= cs;
+  } else {
+    if (w < CW) c.w[w] ^= cs << 16;
+    if (w + 1 < CW) c.w[w + 1] ^= cs >> 16;
+  }
+}
+
+// Recombine leaf values P into c; OFFS is the XOR-set of slot offsets (bit o =
+// offset 16*o) at which the current node's product is added.
+template <int M, int L0, uint32_t OFFS, int K, int CW>
+__device__ __forceinline__ void kara_fin(const uint32_t (&P)[K], Wide<CW>& c) {
+  if constexpr (M == 1) {
+#pragma unroll
+    for (int o = 0; o < 16; o++)
+      if ((OFFS >> o) & 1u) placed_xor(c, P[L0], o);
+  } else {
+    constexpr int h = (M + 1) / 2;
+    kara_fin<h, L0, OFFS ^ (OFFS << h), K, CW>(P, c);
+    kara_fin<M - h, L0 + kara_leaves(h), (OFFS << h) ^ (OFFS << (2 * h)), K, CW>(P, c);
+    kara_fin<h, L0 + kara_leaves(h) + kara_leaves(M - h), (OFFS << h), K, CW>(P, c);
+  }
+}
+
 template <int Q>
 struct Holes {
   static constexpr int EW = cdiv(Q, 32);       // 32-bit words per element
   static constexpr int NH = cdiv(Q, 16);       // 16-bit halves per element
-  static constexpr int NS = 2 * NH - 1;        // half-product slots
+  static constexpr int K = kara_leaves(NH);    // leaf half products per element
   static constexpr int CW = cdiv(2 * Q - 1, 32);
-  uint32_t acc[NS][3];
+  uint32_t acc[K][3];
 
   __device__ __forceinline__ void init() {
 #pragma unroll
-    for (int s = 0; s < NS; s++) acc[s][0] = acc[s][1] = acc[s][2] = 0u;
+    for (int s = 0; s < K; s++) acc[s][0] = acc[s][1] = acc[s][2] = 0u;
   }
 
   __device__ __forceinline__ void add(const uint32_t (&xw)[EW], const uint32_t (&yw)[EW]) {
-    uint32_t xs[NH][3], ys[NH][3];
+    uint32_t xo[NH], yo[NH];
 #pragma unroll
     for (int u = 0; u < NH; u++) {
-      const uint32_t xh = (xw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
-      const uint32_t yh = (yw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
-      xs[u][0] = xh & 0x9249u; xs[u][1] = xh & 0x2492u; xs[u][2] = xh & 0x4924u;
-      ys[u][0] = yh & 0x9249u; ys[u][1] = yh & 0x2492u; ys[u][2] = yh & 0x4924u;
+      xo[u] = (xw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+      yo[u] = (yw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
     }
-#pragma unroll
-    for (int u = 0; u < NH; u++) {
-#pragma unroll
-      for (int v = 0; v < NH; v++) {
-        // residue r collects (i, k) with i + k = r (mod 3)
-        acc[u + v][0] ^= (xs[u][0] * ys[v][0]) ^ (xs[u][1] * ys[v][2]) ^ (xs[u][2] * ys[v][1]);
-        acc[u + v][1] ^= (xs[u][0] * ys[v][1]) ^ (xs[u][1] * ys[v][0]) ^ (xs[u][2] * ys[v][2]);
-        acc[u + v][2] ^= (xs[u][0] * ys[v][2]) ^ (xs[u][1] * ys[v][1]) ^ (xs[u][2] * ys[v][0]);
-      }
-    }
+    kara_acc<NH, 0, K>(xo, yo, acc);
   }
 
   __device__ __forceinline__ Wide<CW> unreduced() const {
-    Wide<CW> c = wzero<CW>();
+    uint32_t P[K];
 #pragma unroll
-    for (int s = 0; s < NS; s++) {
-      const uint32_t cs = (acc[s][0] & 0x49249249u) | (acc[s][1] & 0x92492492u) |
-                          (acc[s][2] & 0x24924924u);
-      placed_xor(c, cs, s);  // slot s sits at bit 16*s; cs has <= 31 bits
-    }
+    for (int s = 0; s < K; s++)
+      P[s] = (acc[s][0] & 0x49249249u) | (acc[s][1] & 0x92492492u) | (acc[s][2] & 0x24924924u);
+    Wide<CW> c = wzero<CW>();
+    kara_fin<NH, 0, 1u, K, CW>(P, c);
     return c;
-  }
-
-  static __device__ __forceinline__ void placed_xor(Wide<CW>& c, uint32_t cs, int s) {
-    // xor cs << (16*s) into c; s is a compile-time constant after unrolling
-    const int w = (16 * s) >> 5;
-    if ((s & 1) == 0) {
-      if (w < CW) c.w[w] ^= cs;
-    } else {
-      if (w < CW) c.w[w] ^= cs << 16;
-      if (w + 1 < CW) c.w[w + 1] ^= cs >> 16;
-    }
   }
 };
 
@@ -290,7 +338,7 @@ __device__ __forceinline__ void read_elem(const uint32_t* src, int64_t off, uint
 }
 
 template <int Q, bool STAGED>
-__global__ void __launch_bounds__(256) eq_kernel(const EqArgs a) {
+__global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_kernel(const EqArgs a) {
   extern __shared__ uint32_t smem[];
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
@@ -448,8 +496,10 @@ __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void
   }
 }
 
+// Register-heavy Karatsuba instances (Q >= 33: >= 7 leaves x 3 accumulators)
+// are held to 128 registers so two CTAs (16 warps) share an SM.
 template <int Q, int U>
-__global__ void __launch_bounds__(256) eq_direct_kernel(const DirectArgs a) {
+__global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -471,8 +521,13 @@ __global__ void __launch_bounds__(256) eq_direct_kernel(const DirectArgs a) {
     } else {
       Holes<Q> acc;
       acc.init();
+      if constexpr (Q > 32) {
+#pragma unroll 1
+        for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+      } else {
 #pragma unroll 2
-      for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+        for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+      }
       c = acc.unreduced();
     }
     z = reduce<Q>(c);

@@ -87,3 +87,40 @@ def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit
     if errors:
         raise errors[0]
     return out.tobytes()
+
+
+def distributed_extract(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0,
+                        y_bit0: int = 0, group=None, compute=None, device=None) -> bytes | None:
+    """Multi-process form (one process per GPU, torch.distributed).
+
+    Every rank sees the same run (e.g. a shared capture file or a shared seeded
+    generator) and computes only its contiguous block range ``rank_range``; the
+    packed parts are gathered to rank 0, which returns the concatenated output
+    (other ranks return None).  There is no collective on the data path: the
+    gather moves only the outputs (1/(2n) of the input bytes).
+
+    ``compute`` defaults to :func:`extract_packed` on ``device``; tests inject a
+    stand-in to exercise the range/offset logic on CPU (gloo).
+    """
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    start, cnt = rank_range(count, rank, world)
+    B = q * n
+    part = b""
+    if cnt:
+        xs, ys = x_bit0 + start * B, y_bit0 + start * B
+        fn = compute or (lambda *a, **k: extract_packed(*a, device=device, **k))
+        part = fn(xv[xs // 8:(xs + cnt * B + 7) // 8], yv[ys // 8:(ys + cnt * B + 7) // 8],
+                  q, n, cnt, x_bit0=xs % 8, y_bit0=ys % 8)
+    parts = [None] * world if rank == 0 else None
+    dist.gather_object((start, cnt, part), parts, dst=0, group=group)
+    if rank != 0:
+        return None
+    out = bytearray((count * q + 7) // 8)
+    for s, c, p in parts:
+        if c:
+            ob = s * q // 8
+            out[ob:ob + len(p)] = p
+    return bytes(out)
