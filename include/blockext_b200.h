@@ -53,8 +53,10 @@ int bx_modulus_exponents(int q, int* exps);
  * preserved (boundary words are updated atomically).
  *
  * x, y, out: device pointers, 4-byte aligned.  x_bytes / y_bytes: bytes of
- * valid stream data; the buffers must stay readable up to the next multiple of
- * 4 bytes plus 4 more.  Requires x_bit0 + nblocks*q*n <= 8*x_bytes (same for y).
+ * valid stream data; the buffers must stay readable up to round_up(x_bytes, 16)
+ * + 16 bytes (the TMA-bulk path copies whole 16-byte granules).  16-byte
+ * aligned x and y select the aligned kernels (direct, or persistent TMA-bulk).
+ * Requires x_bit0 + nblocks*q*n <= 8*x_bytes (same for y).
  */
 int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0,
                   const void* y, int64_t y_bytes, int64_t y_bit0,
@@ -62,10 +64,21 @@ int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0,
                   void* out, int64_t out_bit0, void* stream);
 
 /*
+ * Incremental-width extraction (extract_neq): block k (0-based) has width
+ * q1 + k*step (all <= 128) and reads the next (q1 + k*step)*n bits of each
+ * stream, starting at bit 0; outputs are concatenated from bit 0 of out.
+ * Replaces the neq schedule of Extraction._blocks (extractor.py:170-173,
+ * 188-205).  One launch per distinct width.
+ */
+int bx_extract_neq(const void* x, int64_t x_bytes, const void* y, int64_t y_bytes, int q1,
+                   int step, int n, int64_t nblocks, void* out, void* stream);
+
+/*
  * Launch geometry bx_extract_eq would use (for tests, benches and profiling):
  * threads per block-pair group, blocks per CTA tile, staged (1) or direct (0),
  * CTA threads, dynamic shared memory bytes, grid size, and kernel family
- * (bit 0: 0 = diag, 1 = holes; bit 1 set = aligned direct kernel), for
+ * (bit 0: 0 = diag, 1 = holes; bit 1: aligned direct kernel; bit 2:
+ * persistent TMA-bulk staged kernel), for
  * 16-byte aligned buffers starting at bit 0.  Any output pointer may be NULL.
  */
 int bx_launch_info(int q, int n, int64_t nblocks, int* tpb, int* tile, int* staged,

@@ -23,6 +23,7 @@ SIGNATURES = {
     "bx_last_error": (_cp, []),
     "bx_modulus_exponents": (_i32, [_i32, _PI32]),
     "bx_extract_eq": (_i32, [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i64, _vp, _i64, _vp]),
+    "bx_extract_neq": (_i32, [_vp, _i64, _vp, _i64, _i32, _i32, _i32, _i64, _vp, _vp]),
     "bx_launch_info": (_i32, [_i32, _i32, _i64, _PI32, _PI32, _PI32, _PI32, _PI32, _PI64, _PI32]),
     "bx_pack": (_i32, [_vp, _i32, _i32, _i64, _vp, _i64, _vp]),
     "bx_launch_count": (_i64, [_i32]),
@@ -81,7 +82,8 @@ def launch_info(q: int, n: int, nblocks: int) -> dict:
     tpb, tile, staged, threads, smem = (v.value for v in vals[:5])
     return {"tpb": tpb, "tile": tile, "staged": staged, "threads": threads,
             "smem_bytes": smem, "grid": grid.value,
-            "family": ("diag", "holes")[fam.value & 1], "direct": bool(fam.value & 2)}
+            "family": ("diag", "holes")[fam.value & 1], "direct": bool(fam.value & 2),
+            "tma": bool(fam.value & 4)}
 
 
 def launch_count(reset: bool = False) -> int:

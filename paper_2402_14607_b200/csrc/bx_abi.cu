@@ -61,15 +61,16 @@ int bx_launch_info(int q, int n, int64_t nblocks, int* tpb, int* tile, int* stag
   if (n < 1 || nblocks < 0) return fail(BX_EINVAL, "n must be >= 1 and nblocks >= 0");
   // geometry for 16-byte aligned buffers starting at bit 0
   const void* al = reinterpret_cast<const void*>(uintptr_t(256));
-  const bx::LaunchCfg c = bx::direct_ok(q, n, 0, 0, 0, al, al) ? bx::choose_direct(q, n, nblocks)
-                                                               : bx::choose_launch(q, n, nblocks);
+  bx::LaunchCfg c = bx::direct_ok(q, n, 0, 0, 0, al, al) ? bx::choose_direct(q, n, nblocks)
+                                                         : bx::choose_launch(q, n, nblocks);
+  if (!c.direct && c.staged) bx::make_tma(c, q, n, nblocks);
   if (tpb) *tpb = 1 << c.tpb_log2;
   if (tile) *tile = c.tile;
   if (staged) *staged = c.staged;
   if (threads) *threads = c.threads;
   if (smem_bytes) *smem_bytes = (int)c.smem;
   if (grid) *grid = c.grid;
-  if (family) *family = c.family + (c.direct ? 2 : 0);
+  if (family) *family = c.family + (c.direct ? 2 : 0) + (c.tma ? 4 : 0);
   return BX_OK;
 }
 
@@ -89,9 +90,11 @@ int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0, const void* y,
     return fail(BX_EINVAL, "block range overflows");
   if (x_bit0 + nblocks * B > 8 * x_bytes) return fail(BX_EINVAL, "x stream shorter than the block range");
   if (y_bit0 + nblocks * B > 8 * y_bytes) return fail(BX_EINVAL, "y stream shorter than the block range");
-  const bx::LaunchCfg c = bx::direct_ok(q, n, x_bit0, y_bit0, out_bit0, x, y)
-                              ? bx::choose_direct(q, n, nblocks)
-                              : bx::choose_launch(q, n, nblocks);
+  bx::LaunchCfg c = bx::direct_ok(q, n, x_bit0, y_bit0, out_bit0, x, y)
+                        ? bx::choose_direct(q, n, nblocks)
+                        : bx::choose_launch(q, n, nblocks);
+  if (!c.direct && c.staged && ((((uintptr_t)x) | ((uintptr_t)y)) & 15) == 0)
+    bx::make_tma(c, q, n, nblocks);
   if (c.grid > 0x7FFFFFFF) return fail(BX_EINVAL, "too many blocks for one launch");
   bx::EqArgs a;
   a.x = static_cast<const uint32_t*>(x);
@@ -110,6 +113,28 @@ int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0, const void* y,
   cudaError_t e = table()[q - 1](a, c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_extract_eq: ") + cudaGetErrorString(e));
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int bx_extract_neq(const void* x, int64_t x_bytes, const void* y, int64_t y_bytes, int q1,
+                   int step, int n, int64_t nblocks, void* out, void* stream) {
+  if (n < 1 || nblocks < 0 || q1 < 1 || step < 0) return fail(BX_EINVAL, "bad neq schedule");
+  if (nblocks == 0) return BX_OK;
+  const int64_t qlast = (int64_t)q1 + (nblocks - 1) * (int64_t)step;
+  if (qlast > 128) return fail(BX_ERANGE, "block width beyond 128 (reference width-cap)");
+  int64_t in_off = 0, out_off = 0;
+  int64_t k = 0;
+  while (k < nblocks) {
+    // runs of equal width (step == 0: the whole schedule) go out as one launch
+    const int q = (int)(q1 + k * (int64_t)step);
+    const int64_t run = step == 0 ? nblocks : 1;
+    const int rc = bx_extract_eq(x, x_bytes, in_off, y, y_bytes, in_off, q, n, run, out, out_off,
+                                 stream);
+    if (rc) return rc;
+    in_off += run * (int64_t)q * n;
+    out_off += run * q;
+    k += run;
+  }
   return BX_OK;
 }
 

@@ -209,14 +209,37 @@ struct Diag {
 
 // ---------------------------------------------------------- holes (Q >= 9)
 
+// A 16-bit half split into its three residue classes (bits = r mod 3).
+struct Parts {
+  uint32_t p[3];
+};
+
+__device__ __forceinline__ Parts split_lo(uint32_t w) {  // low half of w
+  return Parts{{w & 0x9249u, w & 0x2492u, w & 0x4924u}};
+}
+
+__device__ __forceinline__ Parts pxor(const Parts& a, const Parts& b) {
+  return Parts{{a.p[0] ^ b.p[0], a.p[1] ^ b.p[1], a.p[2] ^ b.p[2]}};
+}
+
 // One 16x16 carry-less half product with nine 32-bit IMADs on holed operands,
 // XOR-accumulated per residue class (see the header comment).
-__device__ __forceinline__ void holes16(uint32_t xh, uint32_t yh, uint32_t (&acc)[3]) {
-  const uint32_t x0 = xh & 0x9249u, x1 = xh & 0x2492u, x2 = xh & 0x4924u;
-  const uint32_t y0 = yh & 0x9249u, y1 = yh & 0x2492u, y2 = yh & 0x4924u;
-  acc[0] ^= (x0 * y0) ^ (x1 * y2) ^ (x2 * y1);
-  acc[1] ^= (x0 * y1) ^ (x1 * y0) ^ (x2 * y2);
-  acc[2] ^= (x0 * y2) ^ (x1 * y1) ^ (x2 * y0);
+__device__ __forceinline__ void holes16(const Parts& x, const Parts& y, uint32_t (&acc)[3]) {
+  acc[0] ^= (x.p[0] * y.p[0]) ^ (x.p[1] * y.p[2]) ^ (x.p[2] * y.p[1]);
+  acc[1] ^= (x.p[0] * y.p[1]) ^ (x.p[1] * y.p[0]) ^ (x.p[2] * y.p[2]);
+  acc[2] ^= (x.p[0] * y.p[2]) ^ (x.p[1] * y.p[1]) ^ (x.p[2] * y.p[0]);
+}
+
+// Two element pairs at once: 18 products into 3 accumulators with 3 three-input
+// LOP3s per residue (instead of 4).
+__device__ __forceinline__ void holes16x2(const Parts& xa, const Parts& ya, const Parts& xb,
+                                          const Parts& yb, uint32_t (&acc)[3]) {
+  acc[0] ^= (xa.p[0] * ya.p[0]) ^ (xa.p[1] * ya.p[2]) ^ (xa.p[2] * ya.p[1]) ^
+            (xb.p[0] * yb.p[0]) ^ (xb.p[1] * yb.p[2]) ^ (xb.p[2] * yb.p[1]);
+  acc[1] ^= (xa.p[0] * ya.p[1]) ^ (xa.p[1] * ya.p[0]) ^ (xa.p[2] * ya.p[2]) ^
+            (xb.p[0] * yb.p[1]) ^ (xb.p[1] * yb.p[0]) ^ (xb.p[2] * yb.p[2]);
+  acc[2] ^= (xa.p[0] * ya.p[2]) ^ (xa.p[1] * ya.p[1]) ^ (xa.p[2] * ya.p[0]) ^
+            (xb.p[0] * yb.p[2]) ^ (xb.p[1] * yb.p[1]) ^ (xb.p[2] * yb.p[0]);
 }
 
 // Karatsuba over 16-bit halves.  A size-M operand pair splits into
@@ -225,29 +248,59 @@ __device__ __forceinline__ void holes16(uint32_t xh, uint32_t yh, uint32_t (&acc
 // Leaves are single half products; they are accumulated over the whole block
 // (all j) and recombined once per block -- the sum over j commutes with the
 // linear recombination, so Karatsuba's extra additions are paid per block,
-// not per element.  Leaves per size: K(1)=1, K(m)=2K(ceil(m/2))+K(floor(m/2))
+// not per element.  Halves are split into residue classes once, and the
+// Mid operands are formed by XOR on the split parts (masking commutes with
+// XOR).  Leaves per size: K(1)=1, K(m)=2K(ceil(m/2))+K(floor(m/2))
 // (K(2)=3, K(4)=9, K(8)=27 vs 4, 16, 64 half products for schoolbook).
 __host__ __device__ constexpr int kara_leaves(int m) {
   return m <= 1 ? 1 : 2 * kara_leaves((m + 1) / 2) + kara_leaves(m / 2);
 }
 
 template <int M, int L0, int K>
-__device__ __forceinline__ void kara_acc(const uint32_t* xo, const uint32_t* yo,
-                                         uint32_t (&acc)[K][3]) {
+__device__ __forceinline__ void kara_acc(const Parts* xo, const Parts* yo, uint32_t (&acc)[K][3]) {
   if constexpr (M == 1) {
     holes16(xo[0], yo[0], acc[L0]);
   } else {
     constexpr int h = (M + 1) / 2;
     kara_acc<h, L0, K>(xo, yo, acc);
     kara_acc<M - h, L0 + kara_leaves(h), K>(xo + h, yo + h, acc);
-    uint32_t xm[h], ym[h];
+    Parts xm[h], ym[h];
 #pragma unroll
     for (int i = 0; i < h; i++) {
-      xm[i] = (i + h < M) ? (xo[i] ^ xo[i + h]) : xo[i];
-      ym[i] = (i + h < M) ? (yo[i] ^ yo[i + h]) : yo[i];
+      xm[i] = (i + h < M) ? pxor(xo[i], xo[i + h]) : xo[i];
+      ym[i] = (i + h < M) ? pxor(yo[i], yo[i + h]) : yo[i];
     }
     kara_acc<h, L0 + kara_leaves(h) + kara_leaves(M - h), K>(xm, ym, acc);
   }
+}
+
+template <int M, int L0, int K>
+__device__ __forceinline__ void kara_acc2(const Parts* xa, const Parts* ya, const Parts* xb,
+                                          const Parts* yb, uint32_t (&acc)[K][3]) {
+  if constexpr (M == 1) {
+    holes16x2(xa[0], ya[0], xb[0], yb[0], acc[L0]);
+  } else {
+    constexpr int h = (M + 1) / 2;
+    kara_acc2<h, L0, K>(xa, ya, xb, yb, acc);
+    kara_acc2<M - h, L0 + kara_leaves(h), K>(xa + h, ya + h, xb + h, yb + h, acc);
+    Parts xam[h], yam[h], xbm[h], ybm[h];
+#pragma unroll
+    for (int i = 0; i < h; i++) {
+      xam[i] = (i + h < M) ? pxor(xa[i], xa[i + h]) : xa[i];
+      yam[i] = (i + h < M) ? pxor(ya[i], ya[i + h]) : ya[i];
+      xbm[i] = (i + h < M) ? pxor(xb[i], xb[i + h]) : xb[i];
+      ybm[i] = (i + h < M) ? pxor(yb[i], yb[i + h]) : yb[i];
+    }
+    kara_acc2<h, L0 + kara_leaves(h) + kara_leaves(M - h), K>(xam, yam, xbm, ybm, acc);
+  }
+}
+
+// Residue-class parts of every 16-bit half of a q-bit element held in EW words
+// (one SHF per word for the high half, three LOP3 per half).
+template <int NH, int EW>
+__device__ __forceinline__ void split_halves(const uint32_t (&w)[EW], Parts (&o)[NH]) {
+#pragma unroll
+  for (int u = 0; u < NH; u++) o[u] = split_lo((u & 1) ? (w[u >> 1] >> 16) : w[u >> 1]);
 }
 
 template <int CW>
@@ -284,6 +337,10 @@ struct Holes {
   static constexpr int NH = cdiv(Q, 16);       // 16-bit halves per element
   static constexpr int K = kara_leaves(NH);    // leaf half products per element
   static constexpr int CW = cdiv(2 * Q - 1, 32);
+  // pairing two elements per accumulate step saves a LOP3 per residue but
+  // doubles the live operand parts; beyond 4 halves it would spill at the
+  // 128-register cap.
+  static constexpr bool kPair = NH <= 4;
   uint32_t acc[K][3];
 
   __device__ __forceinline__ void init() {
@@ -292,13 +349,20 @@ struct Holes {
   }
 
   __device__ __forceinline__ void add(const uint32_t (&xw)[EW], const uint32_t (&yw)[EW]) {
-    uint32_t xo[NH], yo[NH];
-#pragma unroll
-    for (int u = 0; u < NH; u++) {
-      xo[u] = (xw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
-      yo[u] = (yw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
-    }
+    Parts xo[NH], yo[NH];
+    split_halves<NH>(xw, xo);
+    split_halves<NH>(yw, yo);
     kara_acc<NH, 0, K>(xo, yo, acc);
+  }
+
+  __device__ __forceinline__ void add2(const uint32_t (&xa)[EW], const uint32_t (&ya)[EW],
+                                       const uint32_t (&xb)[EW], const uint32_t (&yb)[EW]) {
+    Parts pxa[NH], pya[NH], pxb[NH], pyb[NH];
+    split_halves<NH>(xa, pxa);
+    split_halves<NH>(ya, pya);
+    split_halves<NH>(xb, pxb);
+    split_halves<NH>(yb, pyb);
+    kara_acc2<NH, 0, K>(pxa, pya, pxb, pyb, acc);
   }
 
   __device__ __forceinline__ Wide<CW> unreduced() const {
@@ -337,18 +401,104 @@ __device__ __forceinline__ void read_elem(const uint32_t* src, int64_t off, uint
   if constexpr (Q % 32) w[EW - 1] &= (1u << (Q % 32)) - 1u;
 }
 
-template <int Q, bool STAGED>
-__global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_kernel(const EqArgs a) {
-  extern __shared__ uint32_t smem[];
+// Blocks [tile0, tile0 + nb) of a tile: each group of tpb threads computes one
+// block from the word arrays sx / sy (shared or global memory) whose block 0
+// starts at bit xbase / ybase, and ORs its q-bit output into `so` at bit
+// obase + grp*Q (so must be zeroed).  Ends with the caller's __syncthreads.
+template <int Q>
+__device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx, const uint32_t* sy,
+                                             int64_t xbase, int64_t ybase, uint32_t* so,
+                                             int64_t obase, int nb) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
   const int tpb = 1 << a.tpb_log2;
+  const int64_t B = (int64_t)Q * a.n;
+  const int tid = threadIdx.x;
+  const int grp = tid >> a.tpb_log2, sub = tid & (tpb - 1);
+  Wide<CW> c = wzero<CW>();
+  if (grp < nb) {
+    const int64_t xo = xbase + grp * B, yo = ybase + grp * B;
+    if constexpr (Q <= kDiagMaxQ) {
+      using D = Diag<Q>;
+      D acc;
+      acc.init();
+      const int nch = cdiv(a.n, D::E);
+      for (int ch = sub; ch < nch; ch += tpb) {
+        const int64_t off = (int64_t)ch * D::EB;
+        const int valid = min(D::E, a.n - ch * D::E) * Q;
+        const uint32_t m = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+        acc.add(read32(sx, xo + off) & m, read32(sy, yo + off));
+      }
+      c.w[0] = acc.unreduced();
+    } else {
+      Holes<Q> acc;
+      acc.init();
+      int j = sub;
+      for (; Holes<Q>::kPair && j + tpb < a.n; j += 2 * tpb) {
+        uint32_t xw[EW], yw[EW], xw2[EW], yw2[EW];
+        read_elem<Q>(sx, xo + (int64_t)j * Q, xw);
+        read_elem<Q>(sy, yo + (int64_t)j * Q, yw);
+        read_elem<Q>(sx, xo + (int64_t)(j + tpb) * Q, xw2);
+        read_elem<Q>(sy, yo + (int64_t)(j + tpb) * Q, yw2);
+        acc.add2(xw, yw, xw2, yw2);
+      }
+      for (; j < a.n; j += tpb) {
+        uint32_t xw[EW], yw[EW];
+        read_elem<Q>(sx, xo + (int64_t)j * Q, xw);
+        read_elem<Q>(sy, yo + (int64_t)j * Q, yw);
+        acc.add(xw, yw);
+      }
+      c = acc.unreduced();
+    }
+  }
+  for (int m = 1; m < tpb; m <<= 1) {
+#pragma unroll
+    for (int i = 0; i < CW; i++) c.w[i] ^= __shfl_xor_sync(0xFFFFFFFFu, c.w[i], m);
+  }
+  if (grp < nb && sub == 0) {
+    const Wide<EW> z = reduce<Q>(c);
+    const int64_t ob = obase + (int64_t)grp * Q;
+    const int w0 = (int)(ob >> 5);
+    const uint32_t sh = (uint32_t)(ob & 31);
+#pragma unroll
+    for (int i = 0; i <= EW; i++) {
+      const uint32_t lo = at(z, i - 1), hi = at(z, i);
+      const uint32_t v = sh ? __funnelshift_l(lo, hi, sh) : hi;
+      if (v) atomicOr(&so[w0 + i], v);
+    }
+  }
+}
+
+// Store the assembled output words of one tile: interior words plainly, the
+// (<= 2) boundary words merged atomically so bits outside the run survive.
+__device__ __forceinline__ void tile_store(uint32_t* out, const uint32_t* so, int64_t ostart,
+                                           int64_t oend) {
+  const int64_t gw0 = ostart >> 5;
+  const int ow = (int)(((oend + 31) >> 5) - gw0);
+  for (int i = threadIdx.x; i < ow; i += blockDim.x) {
+    const int64_t lo = (gw0 + i) * 32, hi = lo + 32;
+    const uint32_t v = so[i];
+    if (lo >= ostart && hi <= oend) {
+      out[gw0 + i] = v;
+    } else {
+      const int64_t s = lo > ostart ? lo : ostart;
+      const int64_t e = hi < oend ? hi : oend;
+      const int nbits = (int)(e - s), off = (int)(s - lo);
+      const uint32_t mask = (nbits >= 32 ? 0xFFFFFFFFu : ((1u << nbits) - 1u)) << off;
+      atomicAnd(&out[gw0 + i], ~mask);
+      atomicOr(&out[gw0 + i], v & mask);
+    }
+  }
+}
+
+template <int Q, bool STAGED>
+__global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_kernel(const EqArgs a) {
+  extern __shared__ uint32_t smem[];
   const int T = a.tile_blocks;
   const int64_t B = (int64_t)Q * a.n;
   const int64_t tile0 = (int64_t)blockIdx.x * T;
   const int nb = (int)((a.nblocks - tile0) < T ? (a.nblocks - tile0) : T);
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int grp = tid >> a.tpb_log2, sub = tid & (tpb - 1);
 
   const uint32_t* sx;
   const uint32_t* sy;
@@ -380,69 +530,122 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_kernel(const EqArgs 
   const int ow = (int)((((ostart & 31) + (int64_t)nb * Q + 31) >> 5));
   for (int i = tid; i < ow + 1; i += nthr) so[i] = 0u;
   __syncthreads();
-
-  Wide<CW> c = wzero<CW>();
-  if (grp < nb) {
-    const int64_t xo = xbase + grp * B, yo = ybase + grp * B;
-    if constexpr (Q <= kDiagMaxQ) {
-      using D = Diag<Q>;
-      D acc;
-      acc.init();
-      const int nch = cdiv(a.n, D::E);
-      for (int ch = sub; ch < nch; ch += tpb) {
-        const int64_t off = (int64_t)ch * D::EB;
-        const int valid = min(D::E, a.n - ch * D::E) * Q;
-        const uint32_t m = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
-        acc.add(read32(sx, xo + off) & m, read32(sy, yo + off));
-      }
-      c.w[0] = acc.unreduced();
-    } else {
-      Holes<Q> acc;
-      acc.init();
-      for (int j = sub; j < a.n; j += tpb) {
-        uint32_t xw[EW], yw[EW];
-        read_elem<Q>(sx, xo + (int64_t)j * Q, xw);
-        read_elem<Q>(sy, yo + (int64_t)j * Q, yw);
-        acc.add(xw, yw);
-      }
-      c = acc.unreduced();
-    }
-  }
-  for (int m = 1; m < tpb; m <<= 1) {
-#pragma unroll
-    for (int i = 0; i < CW; i++) c.w[i] ^= __shfl_xor_sync(0xFFFFFFFFu, c.w[i], m);
-  }
-  if (grp < nb && sub == 0) {
-    const Wide<EW> z = reduce<Q>(c);
-    const int64_t ob = (ostart & 31) + (int64_t)grp * Q;
-    const int w0 = (int)(ob >> 5);
-    const uint32_t sh = (uint32_t)(ob & 31);
-#pragma unroll
-    for (int i = 0; i <= EW; i++) {
-      const uint32_t lo = at(z, i - 1), hi = at(z, i);
-      const uint32_t v = sh ? __funnelshift_l(lo, hi, sh) : hi;
-      if (v) atomicOr(&so[w0 + i], v);
-    }
-  }
+  tile_compute<Q>(a, sx, sy, xbase, ybase, so, ostart & 31, nb);
   __syncthreads();
-  const int64_t gw0 = ostart >> 5;
-  const int64_t oend = ostart + (int64_t)nb * Q;
-  for (int i = tid; i < ow; i += nthr) {
-    const int64_t lo = (gw0 + i) * 32, hi = lo + 32;
-    const uint32_t v = so[i];
-    if (lo >= ostart && hi <= oend) {
-      a.out[gw0 + i] = v;
-    } else {
-      const int64_t s = lo > ostart ? lo : ostart;
-      const int64_t e = hi < oend ? hi : oend;
-      const int nbits = (int)(e - s), off = (int)(s - lo);
-      const uint32_t mask = (nbits >= 32 ? 0xFFFFFFFFu : ((1u << nbits) - 1u)) << off;
-      atomicAnd(&a.out[gw0 + i], ~mask);
-      atomicOr(&a.out[gw0 + i], v & mask);
-    }
-  }
+  tile_store(a.out, so, ostart, ostart + (int64_t)nb * Q);
 }
 
+// ------------------------------------------------- TMA-bulk pipelined kernel
+//
+// Persistent CTAs walk tiles t = blockIdx.x, += gridDim.x.  Each tile's two
+// input windows are brought into shared memory with one cp.async.bulk per
+// stream (the TMA engine, completion counted on an mbarrier), double
+// buffered: while the CTA computes tile t from one buffer, tile t + gridDim.x
+// is already landing in the other.  Requires 16-byte aligned stream bases and
+// streams readable through round_up(bytes, 16) + 16.
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+struct TileWin {
+  int64_t lo;      // first byte copied (16-aligned)
+  uint32_t bytes;  // bytes copied (multiple of 16)
+  int64_t bit0;    // bit of block 0 relative to the copied bytes
+};
+
+__device__ __forceinline__ TileWin tile_window(int64_t bit_start, int64_t nbits) {
+  TileWin w;
+  w.lo = (bit_start >> 3) & ~(int64_t)15;
+  const int64_t hi = ((((bit_start + nbits + 7) >> 3) + 4 + 15) & ~(int64_t)15);
+  w.bytes = (uint32_t)(hi - w.lo);
+  w.bit0 = bit_start - 8 * w.lo;
+  return w;
+}
+
+template <int Q>
+__global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_tma_kernel(const EqArgs a) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  const int T = a.tile_blocks;
+  const int sw = a.stage_words;  // words per source buffer (multiple of 4)
+  const int64_t B = (int64_t)Q * a.n;
+  const int64_t ntiles = (a.nblocks + T - 1) / T;
+  const int ow_max = (int)((31 + (int64_t)T * Q + 31) >> 5) + 2;
+  uint32_t* bufs = smem;                          // [stage][x|y][sw]
+  uint32_t* outs = smem + 4 * sw;                 // [stage][ow_max]
+  const char* xg = reinterpret_cast<const char*>(a.x);
+  const char* yg = reinterpret_cast<const char*>(a.y);
+
+  auto issue = [&](int64_t t, int st) {
+    const int64_t tile0 = t * T;
+    const int64_t nb = (a.nblocks - tile0) < T ? (a.nblocks - tile0) : T;
+    const TileWin wx = tile_window(a.x_bit0 + tile0 * B, nb * B);
+    const TileWin wy = tile_window(a.y_bit0 + tile0 * B, nb * B);
+    mbar_expect_tx(&bars[st], wx.bytes + wy.bytes);
+    bulk_g2s(bufs + (2 * st) * sw, xg + wx.lo, wx.bytes, &bars[st]);
+    bulk_g2s(bufs + (2 * st + 1) * sw, yg + wy.lo, wy.bytes, &bars[st]);
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int64_t t = blockIdx.x;
+  if (threadIdx.x == 0 && t < ntiles) issue(t, 0);
+  uint32_t phase[2] = {0u, 0u};
+  int st = 0;
+  for (; t < ntiles; t += gridDim.x, st ^= 1) {
+    const int64_t tn = t + gridDim.x;
+    if (threadIdx.x == 0 && tn < ntiles) issue(tn, st ^ 1);
+    const int64_t tile0 = t * T;
+    const int nb = (int)((a.nblocks - tile0) < T ? (a.nblocks - tile0) : T);
+    const int64_t ostart = a.out_bit0 + tile0 * Q;
+    uint32_t* so = outs + st * ow_max;
+    for (int i = threadIdx.x; i < ow_max; i += blockDim.x) so[i] = 0u;
+    const TileWin wx = tile_window(a.x_bit0 + tile0 * B, (int64_t)nb * B);
+    const TileWin wy = tile_window(a.y_bit0 + tile0 * B, (int64_t)nb * B);
+    mbar_wait(&bars[st], phase[st]);
+    phase[st] ^= 1u;
+    __syncthreads();
+    tile_compute<Q>(a, bufs + (2 * st) * sw, bufs + (2 * st + 1) * sw, wx.bit0, wy.bit0, so,
+                    ostart & 31, nb);
+    __syncthreads();
+    tile_store(a.out, so, ostart, ostart + (int64_t)nb * Q);
+  }
+}
 
 // ------------------------------------------------------- direct kernel
 //
@@ -476,28 +679,35 @@ __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void
     if constexpr (Q == 16) {
 #pragma unroll
       for (int i = 0; i < 4; i++) {
-        uint32_t a0[1] = {xs[i] & 0xFFFFu}, b0[1] = {ys[i] & 0xFFFFu};
-        uint32_t a1[1] = {xs[i] >> 16}, b1[1] = {ys[i] >> 16};
-        acc.add(a0, b0);
-        acc.add(a1, b1);
+        const uint32_t a0[1] = {xs[i]}, b0[1] = {ys[i]};          // low half (split masks it)
+        const uint32_t a1[1] = {xs[i] >> 16}, b1[1] = {ys[i] >> 16};
+        acc.add2(a0, b0, a1, b1);
       }
-    } else {
+    } else if constexpr (4 / EW >= 2 && Holes<Q>::kPair) {
 #pragma unroll
-      for (int e = 0; e < 4 / EW; e++) {
-        uint32_t a[EW], b[EW];
+      for (int e = 0; e < 4 / EW; e += 2) {
+        uint32_t a[EW], b[EW], c2[EW], d2[EW];
 #pragma unroll
         for (int i = 0; i < EW; i++) {
           a[i] = xs[e * EW + i];
           b[i] = ys[e * EW + i];
+          c2[i] = xs[(e + 1) * EW + i];
+          d2[i] = ys[(e + 1) * EW + i];
         }
-        acc.add(a, b);
+        acc.add2(a, b, c2, d2);
       }
+    } else {
+      uint32_t a[EW], b[EW];
+#pragma unroll
+      for (int i = 0; i < EW; i++) {
+        a[i] = xs[i];
+        b[i] = ys[i];
+      }
+      acc.add(a, b);
     }
   }
 }
 
-// Register-heavy Karatsuba instances (Q >= 33: >= 7 leaves x 3 accumulators)
-// are held to 128 registers so two CTAs (16 warps) share an SM.
 template <int Q, int U>
 __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
@@ -521,7 +731,19 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const 
     } else {
       Holes<Q> acc;
       acc.init();
-      if constexpr (Q > 32) {
+      if constexpr (Q == 128 && Holes<Q>::kPair) {
+        // one element per unit: pair consecutive units (elements)
+        int u = 0;
+#pragma unroll 1
+        for (; u + 1 < units; u += 2) {
+          const uint4 X0 = __ldg(xp + u), Y0 = __ldg(yp + u);
+          const uint4 X1 = __ldg(xp + u + 1), Y1 = __ldg(yp + u + 1);
+          const uint32_t a[4] = {X0.x, X0.y, X0.z, X0.w}, b[4] = {Y0.x, Y0.y, Y0.z, Y0.w};
+          const uint32_t c2[4] = {X1.x, X1.y, X1.z, X1.w}, d2[4] = {Y1.x, Y1.y, Y1.z, Y1.w};
+          acc.add2(a, b, c2, d2);
+        }
+        if (u < units) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+      } else if constexpr (Q > 32) {
 #pragma unroll 1
         for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
       } else {

@@ -18,6 +18,7 @@ struct LaunchCfg {
   int64_t grid = 0;
   int family = 0;     // 0 diag, 1 holes
   int direct = 0;     // 1: eq_direct_kernel (aligned fast path)
+  int tma = 0;        // 1: eq_tma_kernel (persistent, cp.async.bulk double buffer)
   int units = 0;      // direct: 128-bit units per block
 };
 
@@ -46,7 +47,7 @@ inline LaunchCfg choose_launch(int q, int n, int64_t nblocks) {
     target = 8;
   } else {
     units = n;
-    target = q <= 32 ? 4 : 2;
+    target = 8;   // amortise the per-thread Karatsuba recombination
   }
   int tpb = 1;
   while (tpb < 32 && units / (2 * tpb) >= target) tpb *= 2;
@@ -87,8 +88,50 @@ inline LaunchCfg choose_direct(int q, int n, int64_t nblocks) {
   return c;
 }
 
+// Persistent TMA-bulk variant of a staged configuration: two stages of both
+// windows (16-byte padded) plus two output tiles; grid = resident CTAs.
+inline int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+inline void make_tma(LaunchCfg& c, int q, int n, int64_t nblocks) {
+  const int64_t B = (int64_t)q * n;
+  auto words = [&](int t) { return (int)((((((int64_t)t * B + 7) >> 3) + 4 + 32) + 15) / 16 * 4); };
+  auto outw = [&](int t) { return (int)((31 + (int64_t)t * q + 31) >> 5) + 2; };
+  auto bytes = [&](int t) { return (size_t)(4 * (int64_t)words(t) + 2 * outw(t)) * 4; };
+  int T = c.tile;
+  const int Tmin = 32 >> c.tpb_log2 > 0 ? 32 >> c.tpb_log2 : 1;
+  while (bytes(T) > 100 * 1024 && T > Tmin) T /= 2;
+  if (bytes(T) > 200 * 1024) return;  // keep the non-pipelined configuration
+  c.tma = 1;
+  c.staged = 1;
+  c.tile = T;
+  c.threads = T << c.tpb_log2;
+  c.stage_words = words(T);
+  c.smem = bytes(T);
+  const int64_t ntiles = (nblocks + T - 1) / T;
+  const int per_sm = (int)((200 * 1024) / c.smem) > 0 ? (int)((200 * 1024) / c.smem) : 1;
+  const int64_t resident = (int64_t)sm_count() * (per_sm < 4 ? per_sm : 4);
+  c.grid = ntiles < resident ? ntiles : resident;
+}
+
 template <int Q>
 cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
+  if (c.tma) {
+    auto k = eq_tma_kernel<Q>;
+    if (c.smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+      if (e != cudaSuccess) return e;
+    }
+    k<<<(unsigned)c.grid, c.threads, c.smem, s>>>(a);
+    return cudaGetLastError();
+  }
   if constexpr (Q == 1 || Q == 2 || Q == 4 || Q == 8 || Q == 16 || Q == 32 || Q == 64 || Q == 128) {
     if (c.direct) {
       DirectArgs d;

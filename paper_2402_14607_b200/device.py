@@ -92,3 +92,17 @@ def pack(samples: torch.Tensor, b: int, *, out: torch.Tensor | None = None, out_
         _lib.check(_lib.lib().bx_pack(samples.data_ptr(), elem, b, count, out.data_ptr(), out_bit0,
                                       stream_ptr(stream, samples.device)), "bx_pack")
     return out
+
+
+def extract_neq(x: torch.Tensor, x_bytes: int, y: torch.Tensor, y_bytes: int, q1: int, step: int,
+                n: int, nblocks: int, *, out: torch.Tensor | None = None,
+                stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Launch bx_extract_neq (widths q1 + k*step) on device buffers."""
+    total = sum(q1 + k * step for k in range(nblocks))
+    if out is None:
+        out = torch.zeros(padded_len((total + 7) // 8), dtype=torch.uint8, device=x.device)
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.lib().bx_extract_neq(x.data_ptr(), x_bytes, y.data_ptr(), y_bytes, q1, step,
+                                             n, nblocks, out.data_ptr(), stream_ptr(stream, x.device)),
+                   "bx_extract_neq")
+    return out

@@ -386,34 +386,60 @@ class Extraction:
         self._stop_reason = "completed" if limit == plan.num_blocks else "block-limit"
 
     def _segments_neq(self) -> Iterator[tuple[int, int, bytes]]:
+        """Incremental widths q_k = q1 + (k-1)*growth*b (extractor.py:170-173).
+
+        growth = 0 runs in bulk segments like eq mode; growth >= 1 stops at the
+        128-bit width cap after <= 128 blocks, so the bookkeeping replays block by
+        block and the device computes all blocks in one bx_extract_neq call."""
         plan = self.plan
         n = plan.vec_len
         limit = self._block_limit()
         step = plan.growth * plan.bits_per_sample
         width = plan.first_field_bits
+        if step == 0:
+            done = 0
+            offset = 0
+            while limit is None or done < limit:
+                if width > MAX_FIELD_BITS:
+                    self._stop_reason = "width-cap"
+                    return
+                cap = self._segment if limit is None else min(self._segment, limit - done)
+                got = self._advance(width, n, cap)
+                if got:
+                    out = self._compute(width, n, got, offset)
+                    self._widths.extend([width] * got)
+                    offset += got * width * n
+                    self._x.release(offset // 8)
+                    self._y.release(offset // 8)
+                    yield done, got, out
+                    done += got
+                if got < cap:
+                    return
+            self._stop_reason = "block-limit"
+            return
         done = 0
-        offset = 0            # stream bit where the next block starts
+        stopped = False
         while limit is None or done < limit:
             if width > MAX_FIELD_BITS:
                 self._stop_reason = "width-cap"
-                return
-            if step:
-                cap = 1       # every block has its own width
-            else:
-                cap = self._segment if limit is None else min(self._segment, limit - done)
-            got = self._advance(width, n, cap)
-            if got:
-                out = self._compute(width, n, got, offset)
-                self._widths.extend([width] * got)
-                offset += got * width * n
-                self._x.release(offset // 8)
-                self._y.release(offset // 8)
-                yield done, got, out
-                done += got
-            if got < cap:
-                return
+                stopped = True
+                break
+            if self._advance(width, n, 1) == 0:
+                stopped = True
+                break
+            self._widths.append(width)
+            done += 1
             width += step
-        self._stop_reason = "block-limit"   # neq has no planned count
+        if not stopped:
+            self._stop_reason = "block-limit"
+        if done:
+            from . import sharding
+
+            total_in = (self._used_bits + 7) // 8
+            out = sharding.extract_neq_packed(self._x.window(0, total_in), self._y.window(0, total_in),
+                                              plan.first_field_bits, step, n, done,
+                                              device=self._device)
+            yield 0, done, out
 
     # -- public protocol
     def _begin(self) -> None:

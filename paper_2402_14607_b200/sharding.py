@@ -47,10 +47,95 @@ def _slice(buf, lo: int, hi: int):
     return buf[lo:hi]
 
 
+PIPE_CHUNK_BYTES = 64 << 20     # host->device pipeline granularity per stream
+
+
+def _as_tensor(buf):
+    """Zero-copy torch view of a host buffer (bytes-like / numpy) or the tensor."""
+    import torch
+
+    if isinstance(buf, torch.Tensor):
+        return buf.reshape(-1).view(torch.uint8)
+    arr = np.frombuffer(memoryview(buf), dtype=np.uint8) if not isinstance(buf, np.ndarray) \
+        else np.ascontiguousarray(buf).reshape(-1).view(np.uint8)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return torch.from_numpy(arr)
+
+
+def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0: int, dev,
+                        out: np.ndarray, out_byte0: int) -> None:
+    """`count` blocks on one device.  Host inputs are streamed in ~64 MiB chunks
+    on a copy stream while earlier chunks compute (one launch per chunk); device
+    inputs are used in place (copied once if they lack the guard padding)."""
+    import torch
+
+    from . import device as D
+
+    B = q * n
+    xt, yt = _as_tensor(xv), _as_tensor(yv)
+    xn, yn = (x_bit0 + count * B + 7) // 8, (y_bit0 + count * B + 7) // 8
+    obytes = (count * q + 7) // 8
+    with torch.cuda.device(dev):
+        comp = torch.cuda.current_stream(dev)
+        res = torch.zeros(D.padded_len(obytes), dtype=torch.uint8, device=dev)
+        if xt.is_cuda and yt.is_cuda:
+            xd, _ = D.to_device_stream(xt[:xn], dev)
+            yd, _ = D.to_device_stream(yt[:yn], dev)
+            D.extract_eq(xd, xn, yd, yn, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0, out=res)
+        else:
+            xd = D.empty_stream(xn, dev)
+            yd = D.empty_stream(yn, dev)
+            pinned = xt.is_pinned() and yt.is_pinned()
+            copy = torch.cuda.Stream(dev) if pinned else comp
+            step = max(ALIGN_BLOCKS, (PIPE_CHUNK_BYTES * 8 // B) // ALIGN_BLOCKS * ALIGN_BLOCKS)
+            done = 0
+            while done < count:
+                cnt = min(step, count - done)
+                xs, ys = x_bit0 + done * B, y_bit0 + done * B
+                xlo, xhi = xs // 8, (xs + cnt * B + 7) // 8
+                ylo, yhi = ys // 8, (ys + cnt * B + 7) // 8
+                with torch.cuda.stream(copy):
+                    xd[xlo:xhi].copy_(xt[xlo:xhi], non_blocking=pinned)
+                    yd[ylo:yhi].copy_(yt[ylo:yhi], non_blocking=pinned)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+                comp.wait_event(ev)
+                D.extract_eq(xd, xn, yd, yn, q, n, cnt, x_bit0=xs, y_bit0=ys, out=res,
+                             out_bit0=done * q, stream=comp)
+                done += cnt
+            if copy is not comp:
+                xd.record_stream(copy)
+                yd.record_stream(copy)
+        out[out_byte0:out_byte0 + obytes] = res[:obytes].cpu().numpy()
+
+
+def extract_neq_packed(xv, yv, q1: int, step: int, n: int, count: int, *, device=None) -> bytes:
+    """Packed output of `count` incremental-width blocks (widths q1 + k*step)
+    read from bit 0 of xv / yv: one H2D of the consumed prefix, one
+    bx_extract_neq call, one D2H."""
+    import torch
+
+    from . import device as D
+
+    dev = D.require_cuda(device)
+    total_in = sum((q1 + k * step) * n for k in range(count))
+    total_out = sum(q1 + k * step for k in range(count))
+    nb = (total_in + 7) // 8
+    with torch.cuda.device(dev):
+        xd, xn = D.to_device_stream(_as_tensor(xv)[:nb], dev)
+        yd, yn = D.to_device_stream(_as_tensor(yv)[:nb], dev)
+        res = D.extract_neq(xd, xn, yd, yn, q1, step, n, count)
+        return res[:(total_out + 7) // 8].cpu().numpy().tobytes()
+
+
 def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit0: int = 0,
                    device=None, devices=None) -> bytes:
     """Packed output of `count` blocks; xv/yv hold the windows (host buffers or
-    torch tensors) starting at bit x_bit0 / y_bit0 of their first byte."""
+    torch tensors) starting at bit x_bit0 / y_bit0 of their first byte.  With
+    several devices the blocks are split into contiguous 64-aligned ranges, one
+    per device, each driven by its own host thread."""
     from . import device as D
 
     devs = [D.require_cuda(d) for d in devices] if devices else [D.require_cuda(device)]
@@ -61,17 +146,10 @@ def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit
 
     def work(dev, start: int, cnt: int) -> None:
         try:
-            import torch
-
             xs, ys = x_bit0 + start * B, y_bit0 + start * B
-            xd, xn = D.to_device_stream(_slice(xv, xs // 8, (xs + cnt * B + 7) // 8), dev)
-            yd, yn = D.to_device_stream(_slice(yv, ys // 8, (ys + cnt * B + 7) // 8), dev)
-            with torch.cuda.device(dev):
-                res = D.extract_eq(xd, xn, yd, yn, q, n, cnt, x_bit0=xs % 8, y_bit0=ys % 8)
-                nbytes = (cnt * q + 7) // 8
-                host = res[:nbytes].cpu().numpy()
-            ob = start * q // 8
-            out[ob:ob + nbytes] = host
+            _extract_one_device(_slice(xv, xs // 8, (xs + cnt * B + 7) // 8),
+                                _slice(yv, ys // 8, (ys + cnt * B + 7) // 8),
+                                q, n, cnt, xs % 8, ys % 8, dev, out, start * q // 8)
         except BaseException as exc:  # noqa: BLE001 - re-raised on the caller's thread
             errors.append(exc)
 

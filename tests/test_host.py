@@ -28,6 +28,19 @@ def oracle_compute(monkeypatch):
         return coracle.extract_eq(xb, yb, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0)
     monkeypatch.setattr(sharding, "extract_packed", fake)
 
+    def fake_neq(xv, yv, q1, step, n, count, *, device=None):
+        xb = bytes(memoryview(xv).cast("B")) if not hasattr(xv, "numpy") else xv.numpy().tobytes()
+        yb = bytes(memoryview(yv).cast("B")) if not hasattr(yv, "numpy") else yv.numpy().tobytes()
+        acc, pos, off = 0, 0, 0
+        for k in range(count):
+            q = q1 + k * step
+            z = coracle.extract_eq(xb, yb, q, n, 1, x_bit0=off, y_bit0=off)
+            acc |= int.from_bytes(z, "little") << pos
+            pos += q
+            off += q * n
+        return acc.to_bytes((pos + 7) // 8, "little")
+    monkeypatch.setattr(sharding, "extract_neq_packed", fake_neq)
+
 
 def test_header_symbols_exported():
     hdr = (REPO / "include" / "blockext_b200.h").read_text()
@@ -65,7 +78,11 @@ def test_launch_info_geometry():
             assert li["threads"] % 32 == 0 and li["threads"] <= 256
             assert li["family"] == ("diag" if q <= 8 else "holes")
             assert li["direct"] == (q in (1, 2, 4, 8, 16, 32, 64, 128) and q * n % 128 == 0)
-            assert li["grid"] == -(-10_000 // li["tile"])
+            ntiles = -(-10_000 // li["tile"])
+            if li["tma"]:
+                assert 0 < li["grid"] <= ntiles and li["staged"]
+            else:
+                assert li["grid"] == ntiles
 
 
 def test_golden_plans_and_bounds(golden):
