@@ -258,6 +258,22 @@ class _Source:
     def tail_bits(self) -> int:
         return self.avail()
 
+    def bulk_capacity(self, B: int) -> int | None:
+        """Blocks of B bits this in-memory source can still serve, or None if the
+        closed form does not apply (file-like source, or blocks > one read)."""
+        if self._mem is None or B > 8 * READ_CHUNK:
+            return None
+        return (8 * self._total - self.consumed) // B
+
+    def bulk_take(self, B: int, k: int) -> None:
+        """Consume k blocks at once.  Valid when bulk_capacity(B) >= k: with
+        blocks no larger than one 64 KiB read, every refill is exactly one read
+        of READ_CHUNK bytes, so after T consumed bits BitReader has made
+        ceil(T / (8*READ_CHUNK)) reads (bitio.py:35-43)."""
+        self.consumed += k * B
+        reads = -(-self.consumed // (8 * READ_CHUNK))
+        self.buffered = max(self.buffered, min(self._total, reads * READ_CHUNK))
+
     def window(self, byte_lo: int, byte_hi: int):
         """Stream bytes [byte_lo, byte_hi) (all already delivered)."""
         if self._mem is not None:
@@ -331,6 +347,13 @@ class Extraction:
         B = width * n
         x, y = self._x, self._y
         done = 0
+        cx, cy = x.bulk_capacity(B), y.bulk_capacity(B)
+        if cx is not None and cy is not None:
+            k = min(cx, cy) if count_cap is None else min(cx, cy, count_cap)
+            if k > 0:
+                x.bulk_take(B, k)
+                y.bulk_take(B, k)
+                done = k
         while count_cap is None or done < count_cap:
             k = min(x.avail() // B, y.avail() // B)
             if count_cap is not None:
