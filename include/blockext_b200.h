@@ -94,6 +94,35 @@ int bx_launch_info(int q, int n, int64_t nblocks, int* tpb, int* tile, int* stag
 int bx_pack(const void* samples, int elem_bytes, int b, int64_t count,
             void* out, int64_t out_bit0, void* stream);
 
+/* ---- device source simulators ---------------- */
+
+/*
+ * Counter-based Bernoulli(p) bits: stream bit i (i = bit0 .. bit0+nbits-1) is
+ * 1 iff (splitmix64(seed*0xD1B54A32D192ED03 + i) >> 11) < p*2^53.  Writes
+ * ceil(nbits/32) words at out (LSB-first), zero past nbits.  Builder-defined
+ * generator of the config-4 block-Markov masks (no reference counterpart).
+ */
+int bx_bernoulli_bits(void* out, int64_t nbits, double p, uint64_t seed, int64_t bit0,
+                      void* stream);
+
+/* In-place inclusive prefix XOR down the rows of a row-major uint32 matrix
+ * (rows x row_words): row r := row 0 ^ ... ^ row r.  scratch: device buffer of
+ * bx_xor_scan_scratch_bytes(rows, row_words) bytes. */
+int64_t bx_xor_scan_scratch_bytes(int64_t rows, int row_words);
+int bx_xor_scan_rows(void* matrix, int64_t rows, int row_words, void* scratch, void* stream);
+
+/*
+ * Sample path of the reference `markov` source (pkg/src/blockext/sources.py:
+ * 141-152): with cum = row-wise cumulative transition table (2^b x 2^b
+ * doubles, last column forced to 1.0) and host-drawn uniforms u[0..count),
+ * state_i = min(searchsorted(cum[state_{i-1}], u_i, right), 2^b - 1) from
+ * start_state; values (uint16) receive state_1 .. state_count.  Segmented
+ * parallel walk; scratch: bx_markov_scratch_bytes(count, b) bytes.
+ */
+int64_t bx_markov_scratch_bytes(int64_t count, int b);
+int bx_markov_chain(const void* u, int64_t count, const void* cum, int b, int start_state,
+                    void* values, void* scratch, void* stream);
+
 /* Number of kernel launches issued by this thread since the last reset. */
 int64_t bx_launch_count(int reset);
 

@@ -27,6 +27,11 @@ SIGNATURES = {
     "bx_launch_info": (_i32, [_i32, _i32, _i64, _PI32, _PI32, _PI32, _PI32, _PI32, _PI64, _PI32]),
     "bx_pack": (_i32, [_vp, _i32, _i32, _i64, _vp, _i64, _vp]),
     "bx_launch_count": (_i64, [_i32]),
+    "bx_bernoulli_bits": (_i32, [_vp, _i64, ctypes.c_double, ctypes.c_uint64, _i64, _vp]),
+    "bx_xor_scan_scratch_bytes": (_i64, [_i64, _i32]),
+    "bx_xor_scan_rows": (_i32, [_vp, _i64, _i32, _vp, _vp]),
+    "bx_markov_scratch_bytes": (_i64, [_i64, _i32]),
+    "bx_markov_chain": (_i32, [_vp, _i64, _vp, _i32, _i32, _vp, _vp, _vp]),
 }
 
 _lock = threading.Lock()

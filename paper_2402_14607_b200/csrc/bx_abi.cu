@@ -12,6 +12,12 @@
 
 namespace bx {
 cudaError_t launch_pack(const void*, int, int, int64_t, void*, int64_t, cudaStream_t);
+cudaError_t launch_bernoulli(uint32_t*, int64_t, uint64_t, int64_t, double, cudaStream_t);
+int64_t xor_scan_scratch_words(int64_t, int);
+cudaError_t launch_xor_scan(uint32_t*, int64_t, int, uint32_t*, cudaStream_t);
+int64_t markov_scratch_ints(int64_t, int);
+cudaError_t launch_markov(const double*, int64_t, const double*, int, int, uint16_t*, int*,
+                          cudaStream_t);
 
 #define BX_EXTERN_Q(Q) extern template cudaError_t launch_eq<Q>(const EqArgs&, const LaunchCfg&, cudaStream_t);
 #define BX_X8(b) BX_EXTERN_Q(b + 1) BX_EXTERN_Q(b + 2) BX_EXTERN_Q(b + 3) BX_EXTERN_Q(b + 4) \
@@ -151,6 +157,54 @@ int bx_pack(const void* samples, int elem_bytes, int b, int64_t count, void* out
                                   static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_pack: ") + cudaGetErrorString(e));
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int bx_bernoulli_bits(void* out, int64_t nbits, double p, uint64_t seed, int64_t bit0,
+                      void* stream) {
+  if (nbits < 0 || bit0 < 0 || !(p >= 0.0 && p <= 1.0)) return fail(BX_EINVAL, "bad Bernoulli request");
+  if (nbits == 0) return BX_OK;
+  if (!out || ((uintptr_t)out & 3)) return fail(BX_EINVAL, "out must be a 4-byte aligned buffer");
+  cudaError_t e = bx::launch_bernoulli(static_cast<uint32_t*>(out), nbits, seed, bit0, p,
+                                       static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_bernoulli_bits: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int64_t bx_xor_scan_scratch_bytes(int64_t rows, int row_words) {
+  if (rows < 0 || row_words < 1) return fail(BX_EINVAL, "bad matrix shape");
+  return 4 * bx::xor_scan_scratch_words(rows, row_words);
+}
+
+int bx_xor_scan_rows(void* matrix, int64_t rows, int row_words, void* scratch, void* stream) {
+  if (rows < 0 || row_words < 1) return fail(BX_EINVAL, "bad matrix shape");
+  if (rows <= 1) return BX_OK;
+  if (!matrix || !scratch || ((uintptr_t)matrix & 3) || ((uintptr_t)scratch & 3))
+    return fail(BX_EINVAL, "matrix and scratch must be 4-byte aligned device buffers");
+  cudaError_t e = bx::launch_xor_scan(static_cast<uint32_t*>(matrix), rows, row_words,
+                                      static_cast<uint32_t*>(scratch), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_xor_scan_rows: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(3, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int64_t bx_markov_scratch_bytes(int64_t count, int b) {
+  if (count < 0 || b < 1 || b > 16) return fail(BX_EINVAL, "bad markov shape");
+  return 4 * bx::markov_scratch_ints(count, b);
+}
+
+int bx_markov_chain(const void* u, int64_t count, const void* cum, int b, int start_state,
+                    void* values, void* scratch, void* stream) {
+  if (count < 0 || b < 1 || b > 16) return fail(BX_EINVAL, "bits per sample outside 1..16");
+  if (start_state < 0 || start_state >= (1 << b)) return fail(BX_EINVAL, "start state out of range");
+  if (count == 0) return BX_OK;
+  if (!u || !cum || !values || !scratch) return fail(BX_EINVAL, "null buffer");
+  cudaError_t e = bx::launch_markov(static_cast<const double*>(u), count, static_cast<const double*>(cum),
+                                    b, start_state, static_cast<uint16_t*>(values),
+                                    static_cast<int*>(scratch), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_markov_chain: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(3, std::memory_order_relaxed);
   return BX_OK;
 }
 

@@ -106,3 +106,49 @@ def extract_neq(x: torch.Tensor, x_bytes: int, y: torch.Tensor, y_bytes: int, q1
                                              n, nblocks, out.data_ptr(), stream_ptr(stream, x.device)),
                    "bx_extract_neq")
     return out
+
+
+def bernoulli_bits(nbits: int, p: float, seed: int, *, bit0: int = 0, out: torch.Tensor | None = None,
+                   out_byte0: int = 0, device=None, stream=None) -> torch.Tensor:
+    """Counter-based Bernoulli(p) bits [bit0, bit0+nbits) (bx_bernoulli_bits), written at
+    byte out_byte0 of `out` (4-byte aligned offset)."""
+    dev = require_cuda(device) if out is None else out.device
+    if out is None:
+        out = empty_stream((nbits + 7) // 8, dev)
+    if out_byte0 % 4:
+        raise ValueError("out_byte0 must be a multiple of 4")
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().bx_bernoulli_bits(out.data_ptr() + out_byte0, nbits, float(p),
+                                                int(seed) & (2**64 - 1), bit0,
+                                                stream_ptr(stream, dev)), "bx_bernoulli_bits")
+    return out
+
+
+def xor_scan_rows(buf: torch.Tensor, rows: int, row_bytes: int, stream=None) -> torch.Tensor:
+    """In place: row r of the (rows x row_bytes) byte matrix := XOR of rows 0..r."""
+    if row_bytes % 4 or buf.data_ptr() % 4:
+        raise ValueError("rows must be whole, aligned 32-bit words")
+    L = _lib.lib()
+    words = row_bytes // 4
+    scratch = torch.empty(max(4, _lib.check(L.bx_xor_scan_scratch_bytes(rows, words), "scratch")),
+                          dtype=torch.uint8, device=buf.device)
+    with torch.cuda.device(buf.device):
+        _lib.check(L.bx_xor_scan_rows(buf.data_ptr(), rows, words, scratch.data_ptr(),
+                                      stream_ptr(stream, buf.device)), "bx_xor_scan_rows")
+    return buf
+
+
+def markov_chain(u: torch.Tensor, cum: torch.Tensor, b: int, start: int, stream=None) -> torch.Tensor:
+    """Reference markov sample path on the device (bx_markov_chain); int16 states."""
+    if u.dtype != torch.float64 or cum.dtype != torch.float64 or not u.is_cuda or not cum.is_cuda:
+        raise ValueError("u and cum must be float64 CUDA tensors")
+    L = _lib.lib()
+    count = u.numel()
+    vals = torch.empty(count, dtype=torch.int16, device=u.device)
+    scratch = torch.empty(max(4, _lib.check(L.bx_markov_scratch_bytes(count, b), "scratch")),
+                          dtype=torch.uint8, device=u.device)
+    with torch.cuda.device(u.device):
+        _lib.check(L.bx_markov_chain(u.data_ptr(), count, cum.data_ptr(), b, start, vals.data_ptr(),
+                                     scratch.data_ptr(), stream_ptr(stream, u.device)),
+                   "bx_markov_chain")
+    return vals

@@ -486,7 +486,7 @@ class Extraction:
             for first, count, packed in self._segments():
                 widths = ([self.plan.field_bits] * count if self.mode == "eq"
                           else self._widths[first:first + count])
-                val = int.from_bytes(packed, "little")
+                val = int.from_bytes(bytes(packed), "little")
                 pos = 0
                 for k, w in enumerate(widths):
                     bits = (val >> pos) & ((1 << w) - 1)
@@ -520,7 +520,7 @@ class Extraction:
                 if carry_bits == 0 and nbits % 8 == 0:
                     parts.append(packed)
                 else:
-                    carry |= int.from_bytes(packed, "little") << carry_bits
+                    carry |= int.from_bytes(bytes(packed), "little") << carry_bits
                     carry_bits += nbits
                     whole = carry_bits // 8
                     if whole:
@@ -532,7 +532,10 @@ class Extraction:
         if sink is not None:
             if carry_bits:
                 parts.append(carry.to_bytes(1, "little"))
-            sink.write(b"".join(parts))
+            if len(parts) == 1:
+                sink.write(memoryview(parts[0]))
+            else:
+                sink.write(b"".join(bytes(p) for p in parts))
             self.report.pad_bits = (-self._output_bits) % 8
         return self.report
 

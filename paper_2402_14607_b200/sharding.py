@@ -88,7 +88,10 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
             xd = D.empty_stream(xn, dev)
             yd = D.empty_stream(yn, dev)
             pinned = xt.is_pinned() and yt.is_pinned()
-            copy = torch.cuda.Stream(dev) if pinned else comp
+            # x and y chunks travel on two copy streams (two DMA engines) while
+            # the compute stream runs each chunk as soon as both halves landed
+            cx = torch.cuda.Stream(dev) if pinned else comp
+            cy = torch.cuda.Stream(dev) if pinned else comp
             step = max(ALIGN_BLOCKS, (PIPE_CHUNK_BYTES * 8 // B) // ALIGN_BLOCKS * ALIGN_BLOCKS)
             done = 0
             while done < count:
@@ -96,19 +99,23 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
                 xs, ys = x_bit0 + done * B, y_bit0 + done * B
                 xlo, xhi = xs // 8, (xs + cnt * B + 7) // 8
                 ylo, yhi = ys // 8, (ys + cnt * B + 7) // 8
-                with torch.cuda.stream(copy):
+                with torch.cuda.stream(cx):
                     xd[xlo:xhi].copy_(xt[xlo:xhi], non_blocking=pinned)
+                with torch.cuda.stream(cy):
                     yd[ylo:yhi].copy_(yt[ylo:yhi], non_blocking=pinned)
-                    ev = torch.cuda.Event()
-                    ev.record(copy)
-                comp.wait_event(ev)
+                if pinned:
+                    comp.wait_stream(cx)
+                    comp.wait_stream(cy)
                 D.extract_eq(xd, xn, yd, yn, q, n, cnt, x_bit0=xs, y_bit0=ys, out=res,
                              out_bit0=done * q, stream=comp)
                 done += cnt
-            if copy is not comp:
-                xd.record_stream(copy)
-                yd.record_stream(copy)
-        out[out_byte0:out_byte0 + obytes] = res[:obytes].cpu().numpy()
+            if pinned:
+                xd.record_stream(cx)
+                yd.record_stream(cy)
+        host = torch.empty(obytes, dtype=torch.uint8, pin_memory=True)
+        host.copy_(res[:obytes], non_blocking=True)
+        comp.synchronize()
+        out[out_byte0:out_byte0 + obytes] = host.numpy()
 
 
 def extract_neq_packed(xv, yv, q1: int, step: int, n: int, count: int, *, device=None) -> bytes:
@@ -131,7 +138,7 @@ def extract_neq_packed(xv, yv, q1: int, step: int, n: int, count: int, *, device
 
 
 def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit0: int = 0,
-                   device=None, devices=None) -> bytes:
+                   device=None, devices=None) -> np.ndarray:
     """Packed output of `count` blocks; xv/yv hold the windows (host buffers or
     torch tensors) starting at bit x_bit0 / y_bit0 of their first byte.  With
     several devices the blocks are split into contiguous 64-aligned ranges, one
@@ -164,7 +171,7 @@ def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit
             t.join()
     if errors:
         raise errors[0]
-    return out.tobytes()
+    return out
 
 
 def distributed_extract(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0,

@@ -129,19 +129,17 @@ def generate_device(model: SourceModel, count: int, device=None):
             D.pack(vals, b, out=out, out_bit0=s * b)
         return out, nbytes
     if model.kind == "markov":
-        # reference sources.py:141-152: sequential chain (host walk of the draws),
-        # packed on the device
+        # reference sources.py:141-152: u = random(count), then the start state
+        # integers(0, 2^b); the chain itself runs on the device
+        # (bx_markov_chain, segmented parallel walk), then bx_pack.
+        if b > 16:
+            raise ValueError("markov models are limited to b <= 16 on the device")
         cum = np.cumsum(model.table, axis=1)
         cum[:, -1] = 1.0
-        u = rng.random(count)
+        u = torch.from_numpy(rng.random(count)).to(dev)
         state = int(rng.integers(0, 1 << b))
-        vals = np.empty(count, dtype=np.int64)
-        top = (1 << b) - 1
-        for i in range(count):
-            state = min(int(np.searchsorted(cum[state], u[i], side="right")), top)
-            vals[i] = state
-        t = torch.from_numpy(vals).to(dev)
-        D.pack(t, b, out=out)
+        vals = D.markov_chain(u, torch.from_numpy(cum).to(dev), b, state)
+        D.pack(vals, b, out=out)
         return out, nbytes
     raise ValueError(f"cannot generate from a {model.kind!r} model")
 

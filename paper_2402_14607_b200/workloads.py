@@ -213,31 +213,53 @@ def stream_bytes_host(spec: SourceSpec, samples: int, chunk: int = 1 << 24) -> n
     raise ValueError("host streams support b in {1, 8}")
 
 
+SPLITMIX_GAMMA = 0x9E3779B97F4A7C15
+SEED_MIX = 0xD1B54A32D192ED03
+
+
+def splitmix_bits_host(seed: int, bit0: int, nbits: int, p: float) -> np.ndarray:
+    """Host restatement of bx_bernoulli_bits (for tests and small streams):
+    bit i = (splitmix64(seed*SEED_MIX + i) >> 11) < p * 2^53, as 0/1 uint8."""
+    with np.errstate(over="ignore"):
+        z = np.uint64((seed * SEED_MIX) & (2**64 - 1)) + np.arange(bit0, bit0 + nbits, dtype=np.uint64)
+        z = z + np.uint64(SPLITMIX_GAMMA)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    t = p * 2.0**53
+    thr = np.uint64(2**53) if t >= 2.0**53 else np.uint64(max(0, int(t)))
+    return ((z >> np.uint64(11)) < thr).astype(np.uint8)
+
+
 def _block_markov_host(spec: SourceSpec, samples: int) -> np.ndarray:
-    """Block-Markov bit stream (config 4): block 0 ~ uniform bits, block k =
-    block k-1 XOR mask_k with mask bits ~ Bernoulli(flip).  One PCG64 step per
-    bit: the first block's bits, then every later block's mask bits."""
+    """Block-Markov bit stream (config 4), host restatement of the device
+    generator: one counter-based stream of bits (seeded SplitMix64); the first
+    block's bits are Bernoulli(1/2), every later block's bits are
+    Bernoulli(flip) masks, and block k = block k-1 XOR mask_k."""
     B = spec.block_bits
     if B % 64 or samples % B:
         raise ValueError("block-markov needs 64-bit-multiple blocks dividing the stream")
     nblocks = samples // B
-    wpb = B // 64
-    out = np.empty(nblocks * wpb, dtype=np.uint64)
-    rng = np.random.default_rng(spec.seed)
-    prev = np.packbits((rng.random(B) < 0.5).astype(np.uint8), bitorder="little").view(np.uint64)
-    out[:wpb] = prev
-    per = max(1, (1 << 22) // B)
-    k = 1
-    while k < nblocks:
-        c = min(per, nblocks - k)
-        masks = np.packbits((rng.random(c * B) < spec.p).astype(np.uint8),
-                            bitorder="little").view(np.uint64).reshape(c, wpb)
-        masks[0] ^= prev
-        chain = np.bitwise_xor.accumulate(masks, axis=0)
-        out[k * wpb:(k + c) * wpb] = chain.reshape(-1)
-        prev = chain[-1].copy()
-        k += c
-    return out.view(np.uint8)
+    first = splitmix_bits_host(spec.seed, 0, B, 0.5)
+    rest = splitmix_bits_host(spec.seed, B, samples - B, spec.p)
+    bits = np.concatenate([first, rest])
+    words = np.packbits(bits, bitorder="little").view(np.uint64).reshape(nblocks, B // 64)
+    return np.bitwise_xor.accumulate(words, axis=0).reshape(-1).view(np.uint8)
+
+
+def _block_markov_device(spec: SourceSpec, samples: int, device=None):
+    from . import device as D
+
+    B = spec.block_bits
+    if B % 64 or samples % B:
+        raise ValueError("block-markov needs 64-bit-multiple blocks dividing the stream")
+    dev = D.require_cuda(device)
+    nbytes = samples // 8
+    out = D.empty_stream(nbytes, dev)
+    D.bernoulli_bits(B, 0.5, spec.seed, bit0=0, out=out)
+    D.bernoulli_bits(samples - B, spec.p, spec.seed, bit0=B, out=out, out_byte0=B // 8)
+    D.xor_scan_rows(out, samples // B, B // 8)
+    return out, nbytes
 
 
 # ---------------------------------------------------------------- device RNG
@@ -259,6 +281,5 @@ def stream_device(spec: SourceSpec, samples: int, device=None):
     from . import sources as S
 
     if spec.kind == "block-markov":
-        host = _block_markov_host(spec, samples)
-        return D.to_device_stream(host, D.require_cuda(device))
+        return _block_markov_device(spec, samples, device)
     return S.generate_device(to_model(spec), samples, device)

@@ -21,6 +21,7 @@ Fixtures:
                   configs (windows regenerated with PCG64 advance)
   streams.json    sha256 of stream prefixes from the reference generate(), pinning
                   paper_2402_14607_b200.workloads against it
+  markov.json     generate(markov(T, b, seed), count) outputs (sources.py:141-152)
 """
 from __future__ import annotations
 
@@ -254,6 +255,22 @@ def make_streams():
     dump("streams.json", out)
 
 
+def markov_table(b: int, table_seed: int) -> np.ndarray:
+    """Transition table used by the markov fixtures (regenerated by the tests)."""
+    size = 1 << b
+    t = np.random.default_rng(table_seed).random((size, size)) ** 3
+    return t / t.sum(axis=1, keepdims=True)
+
+
+def make_markov():
+    cases = []
+    for b, count, seed in [(1, 5000, 3), (2, 4000, 4), (3, 3000, 5), (4, 3000, 6), (8, 2000, 7)]:
+        t = markov_table(b, 31 + b)
+        data = R_src.generate(R_src.markov(t, b, seed=seed), count)
+        cases.append({"b": b, "count": count, "seed": seed, "table_seed": 31 + b, "out": data.hex()})
+    dump("markov.json", cases)
+
+
 def make_sampled():
     out = {}
     rnd = random.Random(4242)
@@ -289,7 +306,7 @@ def make_sampled():
 
 def main(argv):
     which = set(argv[1:]) or {"moduli", "gf", "ext_ip", "eq", "neq", "pack", "c1",
-                              "streams", "sampled"}
+                              "streams", "sampled", "markov"}
     if "moduli" in which:
         make_moduli()
     if "gf" in which:
@@ -308,6 +325,8 @@ def main(argv):
         make_streams()
     if "sampled" in which:
         make_sampled()
+    if "markov" in which:
+        make_markov()
     print("reference blockext", blockext.__version__, file=sys.stderr)
 
 
