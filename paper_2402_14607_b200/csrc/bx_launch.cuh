@@ -129,7 +129,14 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
       if (e != cudaSuccess) return e;
     }
-    k<<<(unsigned)c.grid, c.threads, c.smem, s>>>(a);
+    // persistent: exactly the CTAs that can be resident at once
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c.threads, c.smem);
+    if (e != cudaSuccess) return e;
+    const int64_t ntiles = (a.nblocks + c.tile - 1) / c.tile;
+    const int64_t resident = (int64_t)sm_count() * (occ > 0 ? occ : 1);
+    const int64_t grid = ntiles < resident ? ntiles : resident;
+    k<<<(unsigned)grid, c.threads, c.smem, s>>>(a);
     return cudaGetLastError();
   }
   if constexpr (Q == 1 || Q == 2 || Q == 4 || Q == 8 || Q == 16 || Q == 32 || Q == 64 || Q == 128) {
