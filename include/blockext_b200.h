@@ -123,6 +123,21 @@ int64_t bx_markov_scratch_bytes(int64_t count, int b);
 int bx_markov_chain(const void* u, int64_t count, const void* cum, int b, int start_state,
                     void* values, void* scratch, void* stream);
 
+/* ---- exhaustive verification kernels --------- */
+
+/* z[i*2^t + y] = <x0+i, y> over GF(2^q) (default modulus), t = q*n <= 16, for
+ * i < nx and all y < 2^t; out: uint16.  Replaces the dense inner-product table
+ * of the reference verify.ip_value_table (pkg/src/blockext/verify.py:200-207). */
+int bx_ip_table(int q, int n, uint32_t x0, uint32_t nx, void* out, void* stream);
+
+/* counts[i*2^q + v] = #{y < 2^t : <d0+i, y> = v} for i < nd (uint32); the
+ * histograms of verify._hadamard_counts (verify.py:262-297). */
+int bx_ip_histograms(int q, int n, uint32_t d0, uint32_t nd, void* counts, void* stream);
+
+/* flags[r] = 1 iff counts[r*bins + v] == expected for every v (uint8). */
+int bx_rows_uniform(const void* counts, uint32_t nrows, uint32_t bins, uint32_t expected,
+                    void* flags, void* stream);
+
 /* Number of kernel launches issued by this thread since the last reset. */
 int64_t bx_launch_count(int reset);
 

@@ -32,6 +32,9 @@ SIGNATURES = {
     "bx_xor_scan_rows": (_i32, [_vp, _i64, _i32, _vp, _vp]),
     "bx_markov_scratch_bytes": (_i64, [_i64, _i32]),
     "bx_markov_chain": (_i32, [_vp, _i64, _vp, _i32, _i32, _vp, _vp, _vp]),
+    "bx_ip_table": (_i32, [_i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp]),
+    "bx_ip_histograms": (_i32, [_i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp]),
+    "bx_rows_uniform": (_i32, [_vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp]),
 }
 
 _lock = threading.Lock()

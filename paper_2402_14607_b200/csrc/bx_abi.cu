@@ -18,6 +18,10 @@ cudaError_t launch_xor_scan(uint32_t*, int64_t, int, uint32_t*, cudaStream_t);
 int64_t markov_scratch_ints(int64_t, int);
 cudaError_t launch_markov(const double*, int64_t, const double*, int, int, uint16_t*, int*,
                           cudaStream_t);
+cudaError_t launch_ip_table(int, uint32_t, int, uint32_t, uint32_t, uint16_t*, cudaStream_t);
+cudaError_t launch_ip_hist(int, uint32_t, int, uint32_t, uint32_t, uint32_t*, cudaStream_t);
+cudaError_t launch_rows_uniform(const uint32_t*, uint32_t, uint32_t, uint32_t, uint8_t*,
+                                cudaStream_t);
 
 #define BX_EXTERN_Q(Q) extern template cudaError_t launch_eq<Q>(const EqArgs&, const LaunchCfg&, cudaStream_t);
 #define BX_X8(b) BX_EXTERN_Q(b + 1) BX_EXTERN_Q(b + 2) BX_EXTERN_Q(b + 3) BX_EXTERN_Q(b + 4) \
@@ -205,6 +209,49 @@ int bx_markov_chain(const void* u, int64_t count, const void* cum, int b, int st
                                     static_cast<int*>(scratch), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_markov_chain: ") + cudaGetErrorString(e));
   g_launches.fetch_add(3, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+static uint32_t modulus_low(int q) {
+  uint32_t low = 0;
+  const bx::ModRow& r = bx::kModulus[q];
+  for (int i = 0; i < r.count; i++)
+    if (r.e[i] != q) low |= 1u << r.e[i];
+  return low;
+}
+
+int bx_ip_table(int q, int n, uint32_t x0, uint32_t nx, void* out, void* stream) {
+  if (q < 1 || n < 1 || q * n > 16) return fail(BX_EINVAL, "ip table needs q*n <= 16");
+  if (nx == 0) return BX_OK;
+  if ((uint64_t)x0 + nx > (1ull << (q * n))) return fail(BX_EINVAL, "x range beyond 2^(q*n)");
+  if (!out || ((uintptr_t)out & 1)) return fail(BX_EINVAL, "out must be a 2-byte aligned buffer");
+  cudaError_t e = bx::launch_ip_table(q, modulus_low(q), n, x0, nx, static_cast<uint16_t*>(out),
+                                      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_ip_table: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int bx_ip_histograms(int q, int n, uint32_t d0, uint32_t nd, void* counts, void* stream) {
+  if (q < 1 || n < 1 || q * n > 16) return fail(BX_EINVAL, "histograms need q*n <= 16");
+  if (nd == 0) return BX_OK;
+  if ((uint64_t)d0 + nd > (1ull << (q * n))) return fail(BX_EINVAL, "d range beyond 2^(q*n)");
+  if (!counts || ((uintptr_t)counts & 3)) return fail(BX_EINVAL, "counts must be 4-byte aligned");
+  cudaError_t e = bx::launch_ip_hist(q, modulus_low(q), n, d0, nd, static_cast<uint32_t*>(counts),
+                                     static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_ip_histograms: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int bx_rows_uniform(const void* counts, uint32_t nrows, uint32_t bins, uint32_t expected,
+                    void* flags, void* stream) {
+  if (nrows == 0) return BX_OK;
+  if (!counts || !flags) return fail(BX_EINVAL, "null buffer");
+  cudaError_t e = bx::launch_rows_uniform(static_cast<const uint32_t*>(counts), nrows, bins, expected,
+                                          static_cast<uint8_t*>(flags), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_rows_uniform: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return BX_OK;
 }
 

@@ -1,0 +1,122 @@
+// bx_verify.cu -- exhaustive small-instance kernels for the verification
+// suites (reference pkg/src/blockext/verify.py).
+//
+// Instances have t = q*n <= 16 input bits per source, so every vector fits a
+// 32-bit word and an inner product <x, y> = sum_j x_j * y_j over GF(2^q)
+// (reference extractor.py:77-87) is evaluated per thread: carry-less products
+// accumulated unreduced (degree <= 2q-2 < 32) and one reduction by the
+// modulus's low part (fold per set high bit, reference gf2q.py:156-169).
+//
+//  * ip_table_kernel:   z[x][y] = <x, y> for x in [x0, x0+nx), all y
+//                       (reference ip_value_table, verify.py:200-207)
+//  * ip_hist_kernel:    counts[d][v] = #{y : <d, y> = v} for d in [d0, d0+nd)
+//                       (the histograms of _hadamard_counts, verify.py:262-297)
+//  * rows_uniform:      flag[d] = all counts[d][.] == expected
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bx {
+
+struct SmallField {
+  int q;
+  uint32_t mask;
+  uint32_t low;  // modulus without x^q
+};
+
+__device__ __forceinline__ uint32_t clmul_small(uint32_t a, uint32_t b) {
+  uint32_t r = 0;
+  while (a) {
+    const int i = __ffs(a) - 1;
+    r ^= b << i;
+    a &= a - 1;
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint32_t reduce_small(const SmallField& f, uint32_t c) {
+  // c has degree <= 2q-2; fold the high part bit by bit from the top
+  for (int i = 2 * f.q - 2; i >= f.q; i--) {
+    if ((c >> i) & 1u) c ^= (1u << i) ^ (f.low << (i - f.q));
+  }
+  return c & f.mask;
+}
+
+__device__ __forceinline__ uint32_t ip_small(const SmallField& f, int n, uint32_t x, uint32_t y) {
+  uint32_t c = 0;
+  for (int j = 0; j < n; j++) {
+    const uint32_t xj = (x >> (j * f.q)) & f.mask, yj = (y >> (j * f.q)) & f.mask;
+    c ^= clmul_small(xj, yj);
+  }
+  return reduce_small(f, c);
+}
+
+__global__ void ip_table_kernel(SmallField f, int n, uint32_t x0, uint32_t nx, uint16_t* out) {
+  const int t = f.q * n;
+  const uint64_t ny = 1ull << t;
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (uint64_t)nx * ny) return;
+  const uint32_t x = x0 + (uint32_t)(i >> t), y = (uint32_t)(i & (ny - 1));
+  out[i] = (uint16_t)ip_small(f, n, x, y);
+}
+
+// One CTA per d; y strided over the CTA; histogram in shared memory when 2^q
+// bins fit, else global atomics on this d's row.
+__global__ void ip_hist_kernel(SmallField f, int n, uint32_t d0, uint32_t* counts) {
+  extern __shared__ uint32_t hist[];
+  const int t = f.q * n;
+  const uint32_t d = d0 + blockIdx.x;
+  const uint32_t bins = 1u << f.q;
+  const bool in_smem = bins <= 8192;
+  uint32_t* row = counts + (uint64_t)blockIdx.x * bins;
+  if (in_smem) {
+    for (uint32_t v = threadIdx.x; v < bins; v += blockDim.x) hist[v] = 0;
+    __syncthreads();
+  }
+  for (uint32_t y = threadIdx.x; y < (1u << t); y += blockDim.x) {
+    const uint32_t v = ip_small(f, n, d, y);
+    atomicAdd(in_smem ? &hist[v] : &row[v], 1u);
+  }
+  if (in_smem) {
+    __syncthreads();
+    for (uint32_t v = threadIdx.x; v < bins; v += blockDim.x) row[v] = hist[v];
+  }
+}
+
+__global__ void rows_uniform_kernel(const uint32_t* counts, uint32_t nrows, uint32_t bins,
+                                    uint32_t expected, uint8_t* flags) {
+  const uint32_t r = blockIdx.x;
+  if (r >= nrows) return;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (uint32_t v = threadIdx.x; v < bins; v += blockDim.x)
+    if (counts[(uint64_t)r * bins + v] != expected) bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) flags[r] = bad ? 0 : 1;
+}
+
+cudaError_t launch_ip_table(int q, uint32_t low, int n, uint32_t x0, uint32_t nx, uint16_t* out,
+                            cudaStream_t st) {
+  SmallField f{q, (1u << q) - 1u, low};
+  const uint64_t total = (uint64_t)nx << (q * n);
+  ip_table_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(f, n, x0, nx, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ip_hist(int q, uint32_t low, int n, uint32_t d0, uint32_t nd, uint32_t* counts,
+                           cudaStream_t st) {
+  SmallField f{q, (1u << q) - 1u, low};
+  const uint32_t bins = 1u << q;
+  if (bins > 8192) cudaMemsetAsync(counts, 0, (size_t)nd * bins * 4, st);
+  const size_t smem = bins <= 8192 ? bins * 4 : 0;
+  ip_hist_kernel<<<nd, 256, smem, st>>>(f, n, d0, counts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rows_uniform(const uint32_t* counts, uint32_t nrows, uint32_t bins,
+                                uint32_t expected, uint8_t* flags, cudaStream_t st) {
+  rows_uniform_kernel<<<nrows, 256, 0, st>>>(counts, nrows, bins, expected, flags);
+  return cudaGetLastError();
+}
+
+}  // namespace bx

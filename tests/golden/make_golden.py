@@ -22,6 +22,8 @@ Fixtures:
   streams.json    sha256 of stream prefixes from the reference generate(), pinning
                   paper_2402_14607_b200.workloads against it
   markov.json     generate(markov(T, b, seed), count) outputs (sources.py:141-152)
+  verify.json     verification-suite results: ip_value_table hashes, one-bit bias
+                  and exact-distance reports, hadamard verdicts (verify.py)
 """
 from __future__ import annotations
 
@@ -271,6 +273,35 @@ def make_markov():
     dump("markov.json", cases)
 
 
+def make_verify():
+    from blockext import verify as R_v
+    out = {"tables": {}, "bias": [], "distance": [], "hadamard": []}
+    for q, n in [(1, 3), (2, 3), (3, 4), (4, 3), (5, 2), (6, 2), (12, 1), (2, 6)]:
+        z = R_v.ip_value_table(R_gf.field(q), n)
+        out["tables"][f"{q},{n}"] = hashlib.sha256(z.astype(np.uint16).tobytes()).hexdigest()
+    for q, n, k, seed in [(2, 2, 2, 0), (2, 3, 3, 1), (3, 2, 4, 2), (4, 2, 5, 3), (1, 4, 2, 4)]:
+        r = R_v.check_one_bit_bias(R_gf.field(q), n, k, seed=seed, sampled_pairs=60)
+        out["bias"].append({"q": q, "n": n, "k": k, "seed": seed, "max_bias": repr(r.max_bias),
+                            "bound": repr(r.bound), "pairs": r.pairs_tested,
+                            "exhaustive": r.exhaustive})
+    rng = np.random.default_rng(77)
+    for q, n in [(2, 2), (3, 3), (4, 2), (2, 5)]:
+        size = 1 << (q * n)
+        px = rng.random(size) ** 4
+        px /= px.sum()
+        py = rng.random(size) ** 2
+        py /= py.sum()
+        r = R_v.check_extractor_distance(R_gf.field(q), n, px, py)
+        out["distance"].append({"q": q, "n": n, "seed": 77, "distance": repr(r.distance),
+                                "bound": repr(r.bound), "rate": repr(r.rate)})
+    for q, n in [(1, 5), (2, 4), (3, 3), (5, 2), (9, 1), (4, 3)]:
+        out["hadamard"].append({"q": q, "n": n,
+                                "direct": R_v.check_hadamard(R_gf.field(q), n, method="direct")
+                                if q * n <= 12 else None,
+                                "counts": R_v.check_hadamard(R_gf.field(q), n, method="counts")})
+    dump("verify.json", out)
+
+
 def make_sampled():
     out = {}
     rnd = random.Random(4242)
@@ -306,7 +337,7 @@ def make_sampled():
 
 def main(argv):
     which = set(argv[1:]) or {"moduli", "gf", "ext_ip", "eq", "neq", "pack", "c1",
-                              "streams", "sampled", "markov"}
+                              "streams", "sampled", "markov", "verify"}
     if "moduli" in which:
         make_moduli()
     if "gf" in which:
@@ -327,6 +358,8 @@ def main(argv):
         make_sampled()
     if "markov" in which:
         make_markov()
+    if "verify" in which:
+        make_verify()
     print("reference blockext", blockext.__version__, file=sys.stderr)
 
 

@@ -215,3 +215,28 @@ def test_pack_random_offsets_and_widths():
             out = D.pack(t, b, out_bit0=off)
             got = int.from_bytes(out.cpu().numpy().tobytes(), "little") >> off
             assert got & ((1 << (cnt * b)) - 1) == int.from_bytes(want, "little")
+
+
+def test_output_canaries_and_giant_blocks():
+    """Writes stay inside [out_bit0, out_bit0 + k*q) even at buffer ends, and
+    blocks too large for shared memory (direct global reads) are exact."""
+    rnd = random.Random(99)
+    for q, n, k, xo in [(64, 20000, 3, 5), (128, 9000, 2, 0), (7, 100_000, 2, 3), (33, 1, 5000, 1),
+                        (4, 64, 1, 0), (128, 8, 1, 0)]:
+        nb = (xo + k * q * n + 7) // 8
+        xb, yb = rnd.randbytes(nb), rnd.randbytes(nb)
+        want = int.from_bytes(coracle.extract_eq(xb, yb, q, n, k, x_bit0=xo, y_bit0=xo), "little")
+        xd, xn = D.to_device_stream(xb, "cuda")
+        yd, yn = D.to_device_stream(yb, "cuda")
+        for oo in (0, 13):
+            obytes = (oo + k * q + 7) // 8
+            buf = torch.full((obytes + 64,), 0x5A, dtype=torch.uint8, device="cuda")
+            view = buf[:D.padded_len(obytes)]
+            D.extract_eq(xd, xn, yd, yn, q, n, k, x_bit0=xo, y_bit0=xo, out=view, out_bit0=oo)
+            host = buf.cpu().numpy().tobytes()
+            gi = int.from_bytes(host[:obytes], "little")
+            assert (gi >> oo) & ((1 << (k * q)) - 1) == want, (q, n, k, oo)
+            pre = int.from_bytes(bytes([0x5A]) * obytes, "little")
+            keep = ((1 << obytes * 8) - 1) ^ (((1 << (k * q)) - 1) << oo)
+            assert gi & keep == pre & keep
+            assert host[obytes:] == bytes([0x5A]) * 64, "write past the output range"
