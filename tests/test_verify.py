@@ -91,7 +91,9 @@ def test_bias_and_distance_match_reference(golden, cuda):
         py = rng.random(size) ** 2
         py /= py.sum()
         r = V.check_extractor_distance(bx.field(c["q"]), c["n"], px, py)
-        assert r.distance == pytest.approx(float(c["distance"]), rel=1e-12, abs=1e-15)
+        # float64 sums of 2^(2qn) weights in a different order (device scatter-add
+        # vs numpy's sequential bincount); |out - 2^-q| cancels, so compare to 1e-9
+        assert r.distance == pytest.approx(float(c["distance"]), rel=1e-9, abs=1e-15)
         assert repr(r.bound) == c["bound"] and repr(r.rate) == c["rate"]
 
 
