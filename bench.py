@@ -315,6 +315,20 @@ def run_ours(args, wl) -> None:
         e2e_s = float(t.item())
     e2e_ok = sink.getvalue() == host_out and rep.blocks_completed == nblocks
 
+    # same call on pageable `bytes` inputs (the reference's usual stream type):
+    # staged through the pinned ring by host threads
+    xb, yb = xh.tobytes(), yh.tobytes()
+    bx.extract_eq(xb, yb, plan, device=dev).run(io.BytesIO())
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sink_p = io.BytesIO()
+        bx.extract_eq(xb, yb, plan, device=dev).run(sink_p)
+    torch.cuda.synchronize(dev)
+    pageable_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_ok = e2e_ok and sink_p.getvalue() == host_out
+    del xb, yb
+
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -345,6 +359,7 @@ def run_ours(args, wl) -> None:
                     "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": obytes,
                     "output_gbps": world * wl.q * nblocks / e2e_s / 1e9,
                     "seconds_per_step": e2e_s, "steps": e2e_steps,
+                    "pageable_bytes_value": world * 2 * B * nblocks / pageable_s / 1e9,
                     "path": "paper_2402_14607_b200.extract_eq(pinned host tensors).run(BytesIO)",
                     "bit_exact_vs_device_run": e2e_ok},
             "roofline": roofline,

@@ -64,6 +64,55 @@ def _as_tensor(buf):
         return torch.from_numpy(arr)
 
 
+class _Stager:
+    """Pinned host ring for pageable inputs: a slot is filled by host threads
+    (numpy copies release the GIL), then sent with an async H2D on the given
+    stream; a slot is reused only after its previous H2D completed (event)."""
+
+    SLOTS = 4
+    THREADS = 4
+
+    def __init__(self, slot_bytes: int):
+        import concurrent.futures as cf
+
+        import torch
+
+        self.slot_bytes = slot_bytes
+        self._bufs = [torch.empty(slot_bytes, dtype=torch.uint8, pin_memory=True)
+                      for _ in range(self.SLOTS)]
+        self._events = [None] * self.SLOTS
+        self._next = 0
+        self._pool = cf.ThreadPoolExecutor(self.THREADS)
+
+    def copy(self, src, dst, stream) -> None:
+        import torch
+
+        n = src.numel()
+        if n > self.slot_bytes:
+            raise ValueError("chunk larger than a staging slot")
+        k = self._next
+        self._next = (k + 1) % self.SLOTS
+        if self._events[k] is not None:
+            self._events[k].synchronize()
+        buf = self._bufs[k][:n]
+        hs, hb = src.numpy(), buf.numpy()
+        parts = max(1, min(self.THREADS, n >> 22))
+        edges = [n * i // parts for i in range(parts + 1)]
+        list(self._pool.map(lambda i: np.copyto(hb[edges[i]:edges[i + 1]], hs[edges[i]:edges[i + 1]]),
+                            range(parts)))
+        with torch.cuda.stream(stream):
+            dst.copy_(buf, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        self._events[k] = ev
+
+    def close(self) -> None:
+        for ev in self._events:
+            if ev is not None:
+                ev.synchronize()
+        self._pool.shutdown(wait=True)
+
+
 def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0: int, dev,
                         out: np.ndarray, out_byte0: int) -> None:
     """`count` blocks on one device.  Host inputs are streamed in ~64 MiB chunks
@@ -89,29 +138,40 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
             yd = D.empty_stream(yn, dev)
             pinned = xt.is_pinned() and yt.is_pinned()
             # x and y chunks travel on two copy streams (two DMA engines) while
-            # the compute stream runs each chunk as soon as both halves landed
-            cx = torch.cuda.Stream(dev) if pinned else comp
-            cy = torch.cuda.Stream(dev) if pinned else comp
+            # the compute stream runs each chunk as soon as both halves landed;
+            # pageable inputs are first staged through a pinned ring by host
+            # threads (see _Stager) so their H2D is asynchronous too
+            cx = torch.cuda.Stream(dev)
+            cy = torch.cuda.Stream(dev)
+            stager = None if pinned else _Stager(PIPE_CHUNK_BYTES // 2)
             step = max(ALIGN_BLOCKS, (PIPE_CHUNK_BYTES * 8 // B) // ALIGN_BLOCKS * ALIGN_BLOCKS)
+            if stager is not None:
+                step = max(ALIGN_BLOCKS, (stager.slot_bytes * 8 // B - 16) // ALIGN_BLOCKS * ALIGN_BLOCKS)
             done = 0
-            while done < count:
-                cnt = min(step, count - done)
-                xs, ys = x_bit0 + done * B, y_bit0 + done * B
-                xlo, xhi = xs // 8, (xs + cnt * B + 7) // 8
-                ylo, yhi = ys // 8, (ys + cnt * B + 7) // 8
-                with torch.cuda.stream(cx):
-                    xd[xlo:xhi].copy_(xt[xlo:xhi], non_blocking=pinned)
-                with torch.cuda.stream(cy):
-                    yd[ylo:yhi].copy_(yt[ylo:yhi], non_blocking=pinned)
-                if pinned:
+            try:
+                while done < count:
+                    cnt = min(step, count - done)
+                    xs, ys = x_bit0 + done * B, y_bit0 + done * B
+                    xlo, xhi = xs // 8, (xs + cnt * B + 7) // 8
+                    ylo, yhi = ys // 8, (ys + cnt * B + 7) // 8
+                    if stager is None:
+                        with torch.cuda.stream(cx):
+                            xd[xlo:xhi].copy_(xt[xlo:xhi], non_blocking=True)
+                        with torch.cuda.stream(cy):
+                            yd[ylo:yhi].copy_(yt[ylo:yhi], non_blocking=True)
+                    else:
+                        stager.copy(xt[xlo:xhi], xd[xlo:xhi], cx)
+                        stager.copy(yt[ylo:yhi], yd[ylo:yhi], cy)
                     comp.wait_stream(cx)
                     comp.wait_stream(cy)
-                D.extract_eq(xd, xn, yd, yn, q, n, cnt, x_bit0=xs, y_bit0=ys, out=res,
-                             out_bit0=done * q, stream=comp)
-                done += cnt
-            if pinned:
-                xd.record_stream(cx)
-                yd.record_stream(cy)
+                    D.extract_eq(xd, xn, yd, yn, q, n, cnt, x_bit0=xs, y_bit0=ys, out=res,
+                                 out_bit0=done * q, stream=comp)
+                    done += cnt
+            finally:
+                if stager is not None:
+                    stager.close()
+            xd.record_stream(cx)
+            yd.record_stream(cy)
         host = torch.empty(obytes, dtype=torch.uint8, pin_memory=True)
         host.copy_(res[:obytes], non_blocking=True)
         comp.synchronize()
