@@ -70,7 +70,7 @@ class _Stager:
     stream; a slot is reused only after its previous H2D completed (event)."""
 
     SLOTS = 4
-    THREADS = 4
+    THREADS = 8
 
     def __init__(self, slot_bytes: int):
         import concurrent.futures as cf

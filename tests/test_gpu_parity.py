@@ -240,3 +240,14 @@ def test_output_canaries_and_giant_blocks():
             keep = ((1 << obytes * 8) - 1) ^ (((1 << (k * q)) - 1) << oo)
             assert gi & keep == pre & keep
             assert host[obytes:] == bytes([0x5A]) * 64, "write past the output range"
+
+
+def test_bitio_pack_values_round_trip():
+    from paper_2402_14607_b200.bitio import pack_values, unpack_values
+    rnd = random.Random(12)
+    for width in (1, 3, 11, 33, 64, 80, 128):
+        vals = [rnd.getrandbits(width) for _ in range(57)]
+        data, pad = pack_values(vals, width)
+        assert len(data) * 8 == width * len(vals) + pad
+        assert unpack_values(data, width, len(vals)) == vals
+        assert data == coracle.pack(vals, width)

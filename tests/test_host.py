@@ -213,3 +213,29 @@ def test_no_cpu_fallback_without_gpu():
         bx.extract_eq(bytes(100), bytes(100), plan).run()
     with pytest.raises(bx.DeviceError):
         bx.ext_ip(bx.field(4), (1,), (2,))
+
+
+def test_bitio_reader_writer():
+    from paper_2402_14607_b200.bitio import BitReader, BitWriter, unpack_values
+    from bxtest_util import DribbleIO
+    r = BitReader(bytes([0b10110010]))
+    assert [r.read_bits(1) for _ in range(8)] == [0, 1, 0, 0, 1, 1, 0, 1]
+    r = BitReader(bytes([0xAB, 0xCD]))
+    assert r.read_bits(12) == 0xDAB and r.read_bits(4) == 0xC and r.read_bits(1) is None
+    r = BitReader(bytes([0xFF]))
+    assert r.read_bits(5) == 0b11111 and r.read_bits(5) is None
+    assert r.tail_bits() == 3 and r.bits_consumed == 5
+    data = bytes(range(40))
+    a, b = BitReader(data), BitReader(DribbleIO(data, 3))
+    while True:
+        va, vb = a.read_bits(13), b.read_bits(13)
+        assert va == vb
+        if va is None:
+            assert a.tail_bits() == b.tail_bits()
+            break
+    w = BitWriter()
+    w.write_bits(0b101, 3)
+    assert w.getvalue() == (bytes([0b101]), 5)
+    with pytest.raises(ValueError):
+        w.write_bits(4, 2)
+    assert unpack_values(bytes([0x21, 0x43]), 4, 4) == [1, 2, 3, 4]
