@@ -17,5 +17,9 @@ from .gf2q import (MAX_FIELD_BITS, MODULUS_EXPONENTS, GFContext, field, gf_add, 
 from .params import (EqPlan, NeqPlan, error_bound_block, error_bound_eq, error_bound_neq,
                      extraction_rate, plan_eq, plan_neq)
 from .report import ExtractionReport, plan_from_text, plan_to_text
+from .sources import SourceModel, file_source, generate, iid_biased, iid_table, markov
+from .verify import (BiasReport, DistanceReport, check_extractor_distance,
+                     check_first_bit_bijection, check_hadamard, check_one_bit_bias,
+                     check_xor_lemma_instance, hadamard_instances)
 
 __version__ = "0.1.0"
