@@ -43,6 +43,9 @@ REPO = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
 METRIC = "extracted output Gbps and raw input Gbps per GPU at 1/2/4/8 B200; % HBM roofline"
+# measured LOP3 issue rate on this pool's B200 (profiles/r01_pipes_microbench.txt)
+LOP3_PER_S = 18.40e12
+LOP3_SOURCE = "measured LOP3 rate 18.40 T/s x 32 pairs (profiles/r01_pipes_microbench.txt)"
 UNIT = "Gbit/s raw input (both sources, whole job)"
 
 
@@ -280,13 +283,26 @@ def run_ours(args, wl) -> None:
     raw_gbps = world * 2 * B * nblocks / (ms_step * 1e-3) / 1e9
     out_gbps = world * wl.q * nblocks / (ms_step * 1e-3) / 1e9
 
-    # ---- roofline of the (single) kernel: algorithmic bytes per launch
+    # ---- roofline of the (single) kernel: algorithmic bytes per launch, and the
+    # integer roofline: n*q^2 AND-XOR pairs per block at the measured
+    # LOP3 rate x 32 pairs per LOP3; the slower of the two binds
     alg_bytes = nblocks * (2 * B / 8 + wl.q / 8)
     peak, peak_src = _peaks()
     achieved = alg_bytes / (ms_step * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": _traffic(wl.name),
-                "peak_source": peak_src,
+    pairs = nblocks * wl.n * wl.q * wl.q
+    int_peak = LOP3_PER_S * 32 / 1e12
+    int_achieved = pairs / (ms_step * 1e-3) / 1e12
+    hbm_bound = alg_bytes / (peak * 1e9) >= pairs / (int_peak * 1e12)
+    roofline = {"bound": "hbm" if hbm_bound else "int",
+                "achieved": achieved if hbm_bound else int_achieved,
+                "peak": peak if hbm_bound else int_peak,
+                "unit": "GB/s" if hbm_bound else "T AND-XOR pairs/s (schoolbook)",
+                "frac": achieved / peak if hbm_bound else int_achieved / int_peak,
+                "traffic": _traffic(wl.name),
+                "peak_source": peak_src if hbm_bound else LOP3_SOURCE,
+                "hbm": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak},
+                "int": {"achieved": int_achieved, "peak": int_peak,
+                        "unit": "T AND-XOR pairs/s", "frac": int_achieved / int_peak},
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "kernel_ms": ms_step, "launch": _lib.launch_info(wl.q, wl.n, nblocks)}
     li = roofline["launch"]

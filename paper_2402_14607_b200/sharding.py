@@ -172,10 +172,9 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
                     stager.close()
             xd.record_stream(cx)
             yd.record_stream(cy)
-        host = torch.empty(obytes, dtype=torch.uint8, pin_memory=True)
-        host.copy_(res[:obytes], non_blocking=True)
+        # D2H straight into this range of the (pinned) result
+        out[out_byte0:out_byte0 + obytes].copy_(res[:obytes], non_blocking=True)
         comp.synchronize()
-        out[out_byte0:out_byte0 + obytes] = host.numpy()
 
 
 def extract_neq_packed(xv, yv, q1: int, step: int, n: int, count: int, *, device=None) -> bytes:
@@ -199,15 +198,18 @@ def extract_neq_packed(xv, yv, q1: int, step: int, n: int, count: int, *, device
 
 def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit0: int = 0,
                    device=None, devices=None) -> np.ndarray:
-    """Packed output of `count` blocks; xv/yv hold the windows (host buffers or
+    """Packed output of `count` blocks (uint8 array over pinned memory; the last
+    byte is zero-padded); xv/yv hold the windows (host buffers or
     torch tensors) starting at bit x_bit0 / y_bit0 of their first byte.  With
     several devices the blocks are split into contiguous 64-aligned ranges, one
     per device, each driven by its own host thread."""
     from . import device as D
 
+    import torch
+
     devs = [D.require_cuda(d) for d in devices] if devices else [D.require_cuda(device)]
     B = q * n
-    out = np.zeros((count * q + 7) // 8, dtype=np.uint8)
+    out = torch.empty((count * q + 7) // 8, dtype=torch.uint8, pin_memory=True)
     ranges = [r for r in shard_ranges(count, len(devs)) if r[1] > 0]
     errors: list[BaseException] = []
 
@@ -231,7 +233,7 @@ def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit
             t.join()
     if errors:
         raise errors[0]
-    return out
+    return out.numpy()       # a view of the pinned buffer (kept alive by the array)
 
 
 def distributed_extract(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0,
