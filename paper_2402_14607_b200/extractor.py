@@ -18,7 +18,6 @@ device memory on long or unbounded inputs.
 """
 from __future__ import annotations
 
-import io
 import time
 from dataclasses import dataclass
 from typing import Iterable, Iterator, Sequence
@@ -26,7 +25,7 @@ from typing import Iterable, Iterator, Sequence
 import numpy as np
 
 from . import params as _params
-from .gf2q import MAX_FIELD_BITS, GFContext, field
+from .gf2q import MAX_FIELD_BITS, GFContext
 from .params import error_bound_eq, error_bound_neq
 from .report import ExtractionReport
 

@@ -20,7 +20,7 @@ Nothing here touches the GPU; the device-side generators live in ``sources``.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 

@@ -1,0 +1,54 @@
+/* Plain-C consumer of the C ABI (include/blockext_b200.h): no Python, no torch.
+ * Allocates device buffers with the CUDA runtime, extracts random blocks for a
+ * few shapes and compares with the CPU oracle library (oracle/_build). */
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <cuda_runtime.h>
+
+#include "blockext_b200.h"
+
+int bxo_extract_eq(const uint8_t*, int64_t, const uint8_t*, int64_t, int, int, int64_t, const int*,
+                   int, uint8_t*, int64_t, int, int);
+
+static uint64_t rng = 88172645463325252ull;
+static uint8_t rb(void) {
+  rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
+  return (uint8_t)rng;
+}
+
+int main(void) {
+  const int shapes[][3] = {{4, 64, 5000}, {128, 8, 700}, {56, 48, 333}, {13, 7, 999}, {1, 24, 64}};
+  int fails = 0;
+  for (unsigned s = 0; s < sizeof shapes / sizeof shapes[0]; s++) {
+    const int q = shapes[s][0], n = shapes[s][1];
+    const int64_t k = shapes[s][2];
+    const int64_t bytes = (k * q * n + 7) / 8;
+    const int64_t alloc = ((bytes + 15) / 16) * 16 + 16;
+    const int64_t obytes = (k * q + 7) / 8;
+    uint8_t *hx = calloc(alloc, 1), *hy = calloc(alloc, 1), *ho = calloc(obytes + 16, 1),
+            *want = calloc(obytes + 16, 1);
+    for (int64_t i = 0; i < bytes; i++) { hx[i] = rb(); hy[i] = rb(); }
+    void *dx, *dy, *dout;
+    cudaMalloc(&dx, alloc); cudaMalloc(&dy, alloc); cudaMalloc(&dout, obytes + 16);
+    cudaMemcpy(dx, hx, alloc, cudaMemcpyHostToDevice);
+    cudaMemcpy(dy, hy, alloc, cudaMemcpyHostToDevice);
+    cudaMemset(dout, 0, obytes + 16);
+    int rc = bx_extract_eq(dx, bytes, 0, dy, bytes, 0, q, n, k, dout, 0, NULL);
+    if (rc) { printf("q=%d n=%d: rc=%d %s\n", q, n, rc, bx_last_error()); fails++; continue; }
+    cudaMemcpy(ho, dout, obytes, cudaMemcpyDeviceToHost);
+    int exps[5];
+    int ne = bx_modulus_exponents(q, exps);
+    bxo_extract_eq(hx, 0, hy, 0, q, n, k, exps, ne, want, 0, 1, 1);
+    int ok = memcmp(ho, want, obytes) == 0;
+    printf("q=%d n=%d blocks=%lld: %s\n", q, n, (long long)k, ok ? "ok" : "MISMATCH");
+    fails += !ok;
+    cudaFree(dx); cudaFree(dy); cudaFree(dout);
+    free(hx); free(hy); free(ho); free(want);
+  }
+  /* error path: field width beyond the cap */
+  if (bx_extract_eq(NULL, 0, 0, NULL, 0, 0, 200, 4, 1, NULL, 0, NULL) != BX_ERANGE) fails++;
+  printf("launches=%lld version=%d fails=%d\n", (long long)bx_launch_count(0), bx_version(), fails);
+  return fails != 0;
+}

@@ -1,6 +1,5 @@
 """CLI parity (reference pkg/tests/test_cli.py patterns): plan printing and exit
 codes on CPU; file round trips through the GPU path under -m gpu."""
-import io
 
 import numpy as np
 import pytest
@@ -9,7 +8,6 @@ import paper_2402_14607_b200 as bx
 from paper_2402_14607_b200.cli import main
 from oracle import coracle
 
-from bxtest_util import case_inputs, tiny_eq_plan
 
 
 def test_params_prints_flagship_plan(capsys):

@@ -13,7 +13,7 @@ from fractions import Fraction
 import pytest
 
 import paper_2402_14607_b200 as bx
-from paper_2402_14607_b200 import _lib, params, sharding
+from paper_2402_14607_b200 import _lib, sharding
 from oracle import coracle
 
 from bxtest_util import DribbleIO, case_inputs, report_dict, tiny_eq_plan

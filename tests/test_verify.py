@@ -2,7 +2,6 @@
 exhaustive kernels on the GPU, both against the reference's recorded results
 (tests/golden/verify.json)."""
 import hashlib
-import itertools
 
 import numpy as np
 import pytest
