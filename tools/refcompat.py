@@ -26,7 +26,12 @@ def prepare() -> None:
     (DST / "conftest.py").write_text(
         "import sys, pathlib\n"
         "sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))\n"
-        "sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent))\n")
+        "sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent))\n"
+        "import torch\n"
+        "if torch.cuda.is_available():  # warm the CUDA context before timed hypothesis cases\n"
+        "    from paper_2402_14607_b200 import device as _D\n"
+        "    _D.pack(torch.zeros(8, dtype=torch.uint8, device='cuda'), 1)\n"
+        "    torch.cuda.synchronize()\n")
     for name in MODULES:
         text = (SRC / name).read_text()
         text = text.replace("from tests.test_bitio import DribbleIO", "from test_bitio import DribbleIO")
