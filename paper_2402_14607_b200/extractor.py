@@ -31,6 +31,7 @@ from .report import ExtractionReport
 
 READ_CHUNK = 1 << 16          # BitReader chunk size (reference bitio.py:25)
 DEFAULT_SEGMENT_BLOCKS = 1 << 24
+FIRST_LAZY_SEGMENT = 4096        # first chunks of an iteration arrive after 4096 blocks
 
 
 @dataclass(frozen=True)
@@ -311,6 +312,7 @@ class Extraction:
         self._device = device
         self._devices = list(devices) if devices else None
         self._segment = max(64, (int(segment_blocks) // 64) * 64)
+        self._lazy = False               # __iter__: grow segments from FIRST_LAZY_SEGMENT
         self._started = False
         self._used_bits = 0
         self._stop_reason = "completed"
@@ -395,7 +397,7 @@ class Extraction:
         B = width * n
         done = 0
         while done < limit:
-            cap = min(self._segment, limit - done)
+            cap = min(self._seg_cap(done), limit - done)
             got = self._advance(width, n, cap)
             if got:
                 out = self._compute(width, n, got, done * B)
@@ -425,7 +427,8 @@ class Extraction:
                 if width > MAX_FIELD_BITS:
                     self._stop_reason = "width-cap"
                     return
-                cap = self._segment if limit is None else min(self._segment, limit - done)
+                seg = self._seg_cap(done)
+                cap = seg if limit is None else min(seg, limit - done)
                 got = self._advance(width, n, cap)
                 if got:
                     out = self._compute(width, n, got, offset)
@@ -472,10 +475,22 @@ class Extraction:
         if self._workers < 1:
             raise ValueError("workers must be >= 1")
 
+    def _seg_cap(self, done: int) -> int:
+        """Blocks in the next segment.  ``run`` uses full segments; iteration
+        starts at FIRST_LAZY_SEGMENT blocks and doubles, so the first chunks of
+        a live stream come out quickly and long runs still use big launches."""
+        if not self._lazy:
+            return self._segment
+        grown = FIRST_LAZY_SEGMENT
+        while grown <= done and grown < self._segment:
+            grown *= 2
+        return min(grown, self._segment)
+
     def _segments(self) -> Iterator[tuple[int, int, bytes]]:
         return self._segments_eq() if self.mode == "eq" else self._segments_neq()
 
     def __iter__(self) -> Iterator[OutputChunk]:
+        self._lazy = True
         try:
             self._begin()
         except ValueError:
