@@ -595,7 +595,7 @@ __device__ __forceinline__ TileWin tile_window(int64_t bit_start, int64_t nbits)
 }
 
 template <int Q>
-__global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_tma_kernel(const EqArgs a) {
+__global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? 3 : 2))) eq_tma_kernel(const EqArgs a) {
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ __align__(8) uint64_t bars[2];
   const int T = a.tile_blocks;

@@ -101,14 +101,26 @@ inline int sm_count() {
   return n;
 }
 
+// Shared memory per TMA CTA: two stages of both windows; kept small enough for
+// three resident CTAs per SM (228 KB) so tile loads of one CTA overlap the
+// integer work of the others.
+inline size_t tma_budget() {
+  static const size_t b = [] {
+    const char* e = getenv("BX_TMA_BUDGET_KB");
+    return (size_t)(e ? atoi(e) : 72) * 1024;
+  }();
+  return b;
+}
+
 inline void make_tma(LaunchCfg& c, int q, int n, int64_t nblocks) {
+  const size_t kTmaBudget = tma_budget();
   const int64_t B = (int64_t)q * n;
   auto words = [&](int t) { return (int)((((((int64_t)t * B + 7) >> 3) + 4 + 32) + 15) / 16 * 4); };
   auto outw = [&](int t) { return (int)((31 + (int64_t)t * q + 31) >> 5) + 2; };
   auto bytes = [&](int t) { return (size_t)(4 * (int64_t)words(t) + 2 * outw(t)) * 4; };
   int T = c.tile;
   const int Tmin = 32 >> c.tpb_log2 > 0 ? 32 >> c.tpb_log2 : 1;
-  while (bytes(T) > 100 * 1024 && T > Tmin) T /= 2;
+  while (bytes(T) > kTmaBudget && T > Tmin) T /= 2;
   if (bytes(T) > 200 * 1024) return;  // keep the non-pipelined configuration
   c.tma = 1;
   c.staged = 1;
