@@ -251,3 +251,21 @@ def test_bitio_pack_values_round_trip():
         assert len(data) * 8 == width * len(vals) + pad
         assert unpack_values(data, width, len(vals)) == vals
         assert data == coracle.pack(vals, width)
+
+
+def test_lazy_iteration_matches_run():
+    """Iteration uses growing segments (4096, 8192, ...); chunks must equal run()."""
+    rnd = random.Random(31)
+    q, n, k = 13, 5, 20_000
+    nb = (k * q * n + 7) // 8
+    xb, yb = rnd.randbytes(nb), rnd.randbytes(nb)
+    plan = tiny_eq_plan(bx, 1, k * q * n, "3/4", n, q)
+    chunks = list(bx.extract_eq(xb, yb, plan))
+    assert len(chunks) == k and [c.index for c in chunks[:2]] == [1, 2]
+    acc = 0
+    for i, c in enumerate(chunks):
+        acc |= c.bits << (i * q)
+    sink = io.BytesIO()
+    bx.extract_eq(xb, yb, plan).run(sink)
+    assert acc.to_bytes(len(sink.getvalue()), "little") == sink.getvalue()
+    assert sink.getvalue() == coracle.extract_eq(xb, yb, q, n, k)
