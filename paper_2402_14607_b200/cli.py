@@ -80,6 +80,13 @@ class _Pair:
         return False
 
 
+def _devices(args) -> dict:
+    """--devices 0,1,2: shard every segment's blocks across these GPUs."""
+    if not getattr(args, "devices", None):
+        return {}
+    return {"devices": [f"cuda:{int(d)}" for d in args.devices.split(",") if d.strip()]}
+
+
 def cmd_params(args) -> int:
     _emit(plan_to_text(_eq_plan(args)), args.report)
     return 0
@@ -94,7 +101,7 @@ def cmd_extract_eq(args) -> int:
         default = usable * 8 // int(args.b)
     plan = _eq_plan(args, default)
     with _Pair(args.x, args.y) as (fx, fy), open(args.out, "wb") as out:
-        report = extract_eq(fx, fy, plan, workers=args.workers).run(out)
+        report = extract_eq(fx, fy, plan, workers=args.workers, **_devices(args)).run(out)
     _emit(report.to_text(), args.report)
     return 0
 
@@ -123,6 +130,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--out", required=True)
     _plan_flags(p, need_n=False)
     p.add_argument("--workers", type=int, default=1)
+    p.add_argument("--devices", help="comma-separated CUDA device indices to shard across")
     p.add_argument("--report")
     p.set_defaults(func=cmd_extract_eq)
     p = sub.add_parser("extract-neq", help="incremental-block extraction")

@@ -59,6 +59,8 @@ def test_extract_eq_files_round_trip(tmp_path, capsys):
     assert main(args + ["--out", str(tmp_path / "o2.bin"), "--report", str(tmp_path / "r2")]) == 0
     o1 = (tmp_path / "o1.bin").read_bytes()
     assert o1 == (tmp_path / "o2.bin").read_bytes()
+    assert main(args + ["--out", str(tmp_path / "o4.bin"), "--devices", "0,0"]) == 0
+    assert (tmp_path / "o4.bin").read_bytes() == o1
     rep = bx.ExtractionReport.from_text((tmp_path / "r1").read_text())
     plan = rep.plan
     want = coracle.extract_eq(xb, yb, plan.field_bits, plan.vec_len, rep.blocks_completed)
