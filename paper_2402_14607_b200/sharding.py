@@ -64,6 +64,20 @@ def _as_tensor(buf):
         return torch.from_numpy(arr)
 
 
+def _device_view(t, nbytes: int, dev):
+    """Use a device tensor in place when it lives on `dev`, is 16-byte aligned
+    and its storage holds the ABI's guard bytes (round_up(n, 16) + 16);
+    otherwise copy it into a padded buffer (one device-to-device pass)."""
+    from . import device as D
+
+    tail = t.untyped_storage().nbytes() - t.storage_offset() * t.element_size()
+    if (t.device == dev and t.data_ptr() % 16 == 0 and t.is_contiguous()
+            and tail >= D.padded_len(nbytes)):
+        return t
+    buf, _ = D.to_device_stream(t[:nbytes], dev)
+    return buf
+
+
 class _Stager:
     """Pinned host ring for pageable inputs: a slot is filled by host threads
     (numpy copies release the GIL), then sent with an async H2D on the given
@@ -130,8 +144,8 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
         comp = torch.cuda.current_stream(dev)
         res = torch.zeros(D.padded_len(obytes), dtype=torch.uint8, device=dev)
         if xt.is_cuda and yt.is_cuda:
-            xd, _ = D.to_device_stream(xt[:xn], dev)
-            yd, _ = D.to_device_stream(yt[:yn], dev)
+            xd = _device_view(xt, xn, dev)
+            yd = _device_view(yt, yn, dev)
             D.extract_eq(xd, xn, yd, yn, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0, out=res)
         else:
             xd = D.empty_stream(xn, dev)

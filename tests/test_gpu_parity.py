@@ -185,7 +185,12 @@ def test_device_tensor_inputs_and_segments():
     want = coracle.extract_eq(xb, yb, q, n, k)
     xt = torch.frombuffer(bytearray(xb), dtype=torch.uint8).cuda()
     yt = torch.frombuffer(bytearray(yb), dtype=torch.uint8).cuda()
-    for src in ((xb, yb), (xt, yt)):
+    # padded device tensors are used in place (zero-copy path)
+    xp = torch.zeros(nb + 64, dtype=torch.uint8, device="cuda")
+    yp = torch.zeros(nb + 64, dtype=torch.uint8, device="cuda")
+    xp[:nb] = xt
+    yp[:nb] = yt
+    for src in ((xb, yb), (xt, yt), (xp[:nb], yp[:nb])):
         for seg in (64, 1000, 1 << 24):
             sink = io.BytesIO()
             bx.extract_eq(*src, plan, segment_blocks=seg).run(sink)
