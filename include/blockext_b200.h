@@ -138,6 +138,12 @@ int bx_ip_histograms(int q, int n, uint32_t d0, uint32_t nd, void* counts, void*
 int bx_rows_uniform(const void* counts, uint32_t nrows, uint32_t bins, uint32_t expected,
                     void* flags, void* stream);
 
+/* Bounds-check violations recorded by a BX_CHECKED build of the library
+ * (libbx_b200_checked.so): synchronises the device, returns the count and
+ * writes (tag, index, bound) of the first one to first[3] if non-NULL;
+ * returns -1 in normal builds. */
+int64_t bx_checked_violations(int reset, int64_t* first);
+
 /* Number of kernel launches issued by this thread since the last reset. */
 int64_t bx_launch_count(int reset);
 

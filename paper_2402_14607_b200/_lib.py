@@ -6,12 +6,16 @@ product entry point raises :class:`ExtensionMissingError`.
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 import threading
 
 from .errors import CapacityError, DeviceError, ExtensionMissingError
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "libbx_b200.so"
+_LIB_DIR = pathlib.Path(__file__).resolve().parent / "_lib"
+#: BX_LIB=checked loads the bounds-checked build (see csrc/bx_core.cuh, BX_CHECK)
+LIB_PATH = _LIB_DIR / ("libbx_b200_checked.so" if os.environ.get("BX_LIB") == "checked"
+                       else "libbx_b200.so")
 
 BX_OK, BX_EINVAL, BX_ECUDA, BX_ERANGE = 0, -1, -2, -3
 
@@ -27,6 +31,7 @@ SIGNATURES = {
     "bx_launch_info": (_i32, [_i32, _i32, _i64, _PI32, _PI32, _PI32, _PI32, _PI32, _PI64, _PI32]),
     "bx_pack": (_i32, [_vp, _i32, _i32, _i64, _vp, _i64, _vp]),
     "bx_launch_count": (_i64, [_i32]),
+    "bx_checked_violations": (_i64, [_i32, _PI64]),
     "bx_bernoulli_bits": (_i32, [_vp, _i64, ctypes.c_double, ctypes.c_uint64, _i64, _vp]),
     "bx_xor_scan_scratch_bytes": (_i64, [_i64, _i32]),
     "bx_xor_scan_rows": (_i32, [_vp, _i64, _i32, _vp, _vp]),
@@ -96,3 +101,10 @@ def launch_info(q: int, n: int, nblocks: int) -> dict:
 
 def launch_count(reset: bool = False) -> int:
     return int(lib().bx_launch_count(1 if reset else 0))
+
+
+def checked_violations(reset: bool = False) -> tuple[int, tuple[int, int, int]]:
+    """(count, (tag, index, bound) of the first) from a BX_CHECKED build; -1 otherwise."""
+    first = (ctypes.c_int64 * 3)()
+    n = int(lib().bx_checked_violations(1 if reset else 0, first))
+    return n, tuple(first)

@@ -22,6 +22,10 @@ CSRC = PKG / "csrc"
 OUT = PKG / "_lib"
 OBJ = OUT / "obj"
 LIB = OUT / "libbx_b200.so"
+# bounds-checked variant (-DBX_CHECKED, relocatable device code for the shared
+# violation counter); loaded when BX_LIB=checked
+OBJ_CHECKED = OUT / "obj_checked"
+LIB_CHECKED = OUT / "libbx_b200_checked.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
@@ -40,11 +44,12 @@ def _headers_mtime() -> float:
     return max((h.stat().st_mtime for h in hs), default=0.0)
 
 
-def _compile(src: pathlib.Path, hdr_mtime: float, verbose: bool) -> pathlib.Path:
-    obj = OBJ / (src.stem + ".o")
+def _compile(src: pathlib.Path, hdr_mtime: float, verbose: bool, checked: bool = False) -> pathlib.Path:
+    obj = (OBJ_CHECKED if checked else OBJ) / (src.stem + ".o")
     if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
         return obj
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    extra = ["-DBX_CHECKED", "-rdc=true"] if checked else []
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -55,23 +60,25 @@ def _compile(src: pathlib.Path, hdr_mtime: float, verbose: bool) -> pathlib.Path
     return obj
 
 
-def build(verbose: bool = False, jobs: int | None = None) -> pathlib.Path:
-    OBJ.mkdir(parents=True, exist_ok=True)
+def build(verbose: bool = False, jobs: int | None = None, checked: bool = False) -> pathlib.Path:
+    obj_dir, lib = (OBJ_CHECKED, LIB_CHECKED) if checked else (OBJ, LIB)
+    obj_dir.mkdir(parents=True, exist_ok=True)
     srcs = sorted(CSRC.glob("*.cu"))
     hm = _headers_mtime()
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
-        objs = list(ex.map(lambda s: _compile(s, hm, verbose), srcs))
+        objs = list(ex.map(lambda s: _compile(s, hm, verbose, checked), srcs))
     newest = max(o.stat().st_mtime for o in objs)
-    if not LIB.exists() or LIB.stat().st_mtime < newest:
-        tmp = LIB.with_suffix(".so.tmp")
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
+    if not lib.exists() or lib.stat().st_mtime < newest:
+        tmp = lib.with_suffix(".so.tmp")
+        cmd = [nvcc(), *ARCH, "-shared", *(["-rdc=true"] if checked else []), "-o", str(tmp),
+               *map(str, objs)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, checked="--checked" in sys.argv))

@@ -37,6 +37,13 @@ constexpr auto make_table(std::integer_sequence<int, Is...>) {
 
 #include <array>
 
+#ifdef BX_CHECKED
+namespace bx {
+__device__ unsigned long long g_violations = 0;
+__device__ long long g_first_violation[3] = {0, 0, 0};
+}  // namespace bx
+#endif
+
 namespace {
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
@@ -120,6 +127,10 @@ int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0, const void* y,
   a.tpb_log2 = c.tpb_log2;
   a.tile_blocks = c.tile;
   a.stage_words = c.stage_words;
+  // ABI guarantee: readable through round_up(bytes, 16) + 16
+  a.x_limit = ((x_bytes + 15) / 16) * 4 + 4;
+  a.y_limit = ((y_bytes + 15) / 16) * 4 + 4;
+  a.out_words = (out_bit0 + nblocks * q + 31) / 32;
   cudaError_t e = table()[q - 1](a, c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_extract_eq: ") + cudaGetErrorString(e));
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -253,6 +264,26 @@ int bx_rows_uniform(const void* counts, uint32_t nrows, uint32_t bins, uint32_t 
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_rows_uniform: ") + cudaGetErrorString(e));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return BX_OK;
+}
+
+int64_t bx_checked_violations(int reset, int64_t* first) {
+#ifdef BX_CHECKED
+  unsigned long long v = 0;
+  long long f[3] = {0, 0, 0};
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&v, bx::g_violations, sizeof v);
+  cudaMemcpyFromSymbol(f, bx::g_first_violation, sizeof f);
+  if (first) for (int i = 0; i < 3; i++) first[i] = f[i];
+  if (reset) {
+    const unsigned long long z = 0;
+    cudaMemcpyToSymbol(bx::g_violations, &z, sizeof z);
+  }
+  return (int64_t)v;
+#else
+  (void)reset;
+  (void)first;
+  return -1;  // not a checked build
+#endif
 }
 
 int64_t bx_launch_count(int reset) {

@@ -43,6 +43,32 @@
 
 namespace bx {
 
+// ---------------------------------------------------------- checked builds
+// With -DBX_CHECKED (libbx_b200_checked.so) every shared / global index is
+// compared with its bound and violations are counted in g_violations (the
+// first one's tag and index are kept) instead of trapping, so a bad access is
+// reported without faulting the GPU.  Normal builds compile the checks away.
+#ifdef BX_CHECKED
+extern __device__ unsigned long long g_violations;
+extern __device__ long long g_first_violation[3];
+__device__ __noinline__ inline void violation(int tag, long long idx, long long bound) {
+  if (atomicAdd(&g_violations, 1ull) == 0ull) {
+    g_first_violation[0] = tag;
+    g_first_violation[1] = idx;
+    g_first_violation[2] = bound;
+  }
+}
+#define BX_CHECK(idx, bound, tag)                                              \
+  do {                                                                          \
+    const long long bx_i_ = (long long)(idx), bx_b_ = (long long)(bound);       \
+    if (bx_i_ < 0 || bx_i_ >= bx_b_) ::bx::violation((tag), bx_i_, bx_b_);      \
+  } while (0)
+#else
+#define BX_CHECK(idx, bound, tag) \
+  do {                            \
+  } while (0)
+#endif
+
 constexpr int kDiagMaxQ = 8;
 
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
@@ -149,8 +175,9 @@ __device__ __forceinline__ Wide<cdiv(Q, 32)> reduce(const Wide<CW>& c) {
 
 // 32 bits of an LSB-first word stream starting at bit `off` (word off>>5 + 1
 // must be readable).
-__device__ __forceinline__ uint32_t read32(const uint32_t* src, int64_t off) {
+__device__ __forceinline__ uint32_t read32(const uint32_t* src, int64_t off, int64_t lim) {
   const int64_t w = off >> 5;
+  BX_CHECK(w + 1, lim, 1);
   return __funnelshift_r(src[w], src[w + 1], (uint32_t)(off & 31));
 }
 
@@ -393,12 +420,16 @@ struct EqArgs {
   int tpb_log2;        // threads per block = 1 << tpb_log2 (<= 32)
   int tile_blocks;     // blocks per CTA
   int stage_words;     // smem words per source (STAGED only)
+  int64_t x_limit;     // words of x the ABI guarantees readable (checked builds)
+  int64_t y_limit;
+  int64_t out_words;   // words of out the run may touch (checked builds)
 };
 
 template <int Q, int EW>
-__device__ __forceinline__ void read_elem(const uint32_t* src, int64_t off, uint32_t (&w)[EW]) {
+__device__ __forceinline__ void read_elem(const uint32_t* src, int64_t off, int64_t lim,
+                                          uint32_t (&w)[EW]) {
 #pragma unroll
-  for (int i = 0; i < EW; i++) w[i] = read32(src, off + 32 * i);
+  for (int i = 0; i < EW; i++) w[i] = read32(src, off + 32 * i, lim);
   if constexpr (Q % 32) w[EW - 1] &= (1u << (Q % 32)) - 1u;
 }
 
@@ -409,7 +440,8 @@ __device__ __forceinline__ void read_elem(const uint32_t* src, int64_t off, uint
 template <int Q>
 __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx, const uint32_t* sy,
                                              int64_t xbase, int64_t ybase, uint32_t* so,
-                                             int64_t obase, int nb) {
+                                             int64_t obase, int nb, int64_t xlim, int64_t ylim,
+                                             int64_t olim) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
   const int tpb = 1 << a.tpb_log2;
@@ -428,7 +460,7 @@ __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx
         const int64_t off = (int64_t)ch * D::EB;
         const int valid = min(D::E, a.n - ch * D::E) * Q;
         const uint32_t m = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
-        acc.add(read32(sx, xo + off) & m, read32(sy, yo + off));
+        acc.add(read32(sx, xo + off, xlim) & m, read32(sy, yo + off, ylim));
       }
       c.w[0] = acc.unreduced();
     } else {
@@ -437,16 +469,16 @@ __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx
       int j = sub;
       for (; Holes<Q>::kPair && j + tpb < a.n; j += 2 * tpb) {
         uint32_t xw[EW], yw[EW], xw2[EW], yw2[EW];
-        read_elem<Q>(sx, xo + (int64_t)j * Q, xw);
-        read_elem<Q>(sy, yo + (int64_t)j * Q, yw);
-        read_elem<Q>(sx, xo + (int64_t)(j + tpb) * Q, xw2);
-        read_elem<Q>(sy, yo + (int64_t)(j + tpb) * Q, yw2);
+        read_elem<Q>(sx, xo + (int64_t)j * Q, xlim, xw);
+        read_elem<Q>(sy, yo + (int64_t)j * Q, ylim, yw);
+        read_elem<Q>(sx, xo + (int64_t)(j + tpb) * Q, xlim, xw2);
+        read_elem<Q>(sy, yo + (int64_t)(j + tpb) * Q, ylim, yw2);
         acc.add2(xw, yw, xw2, yw2);
       }
       for (; j < a.n; j += tpb) {
         uint32_t xw[EW], yw[EW];
-        read_elem<Q>(sx, xo + (int64_t)j * Q, xw);
-        read_elem<Q>(sy, yo + (int64_t)j * Q, yw);
+        read_elem<Q>(sx, xo + (int64_t)j * Q, xlim, xw);
+        read_elem<Q>(sy, yo + (int64_t)j * Q, ylim, yw);
         acc.add(xw, yw);
       }
       c = acc.unreduced();
@@ -465,7 +497,10 @@ __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx
     for (int i = 0; i <= EW; i++) {
       const uint32_t lo = at(z, i - 1), hi = at(z, i);
       const uint32_t v = sh ? __funnelshift_l(lo, hi, sh) : hi;
-      if (v) atomicOr(&so[w0 + i], v);
+      if (v) {
+        BX_CHECK(w0 + i, olim, 2);
+        atomicOr(&so[w0 + i], v);
+      }
     }
   }
 }
@@ -473,12 +508,13 @@ __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx
 // Store the assembled output words of one tile: interior words plainly, the
 // (<= 2) boundary words merged atomically so bits outside the run survive.
 __device__ __forceinline__ void tile_store(uint32_t* out, const uint32_t* so, int64_t ostart,
-                                           int64_t oend) {
+                                           int64_t oend, int64_t out_words) {
   const int64_t gw0 = ostart >> 5;
   const int ow = (int)(((oend + 31) >> 5) - gw0);
   for (int i = threadIdx.x; i < ow; i += blockDim.x) {
     const int64_t lo = (gw0 + i) * 32, hi = lo + 32;
     const uint32_t v = so[i];
+    BX_CHECK(gw0 + i, out_words, 3);
     if (lo >= ostart && hi <= oend) {
       out[gw0 + i] = v;
     } else {
@@ -511,6 +547,8 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_kernel(const EqArgs 
     const int64_t xw0 = xs >> 5, yw0 = ys >> 5;
     const int nwx = (int)((((xs & 31) + nb * B + 31) >> 5) + 1);
     const int nwy = (int)((((ys & 31) + nb * B + 31) >> 5) + 1);
+    BX_CHECK(nwx - 1, sw, 4);
+    BX_CHECK(nwy - 1, sw, 4);
     for (int i = tid; i < nwx; i += nthr)
       smem[i] = (xw0 + i < a.x_words) ? __ldg(a.x + xw0 + i) : 0u;
     for (int i = tid; i < nwy; i += nthr)
@@ -531,9 +569,11 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_kernel(const EqArgs 
   const int ow = (int)((((ostart & 31) + (int64_t)nb * Q + 31) >> 5));
   for (int i = tid; i < ow + 1; i += nthr) so[i] = 0u;
   __syncthreads();
-  tile_compute<Q>(a, sx, sy, xbase, ybase, so, ostart & 31, nb);
+  const int64_t xlim = STAGED ? a.stage_words : a.x_limit;
+  const int64_t ylim = STAGED ? a.stage_words : a.y_limit;
+  tile_compute<Q>(a, sx, sy, xbase, ybase, so, ostart & 31, nb, xlim, ylim, ow + 1);
   __syncthreads();
-  tile_store(a.out, so, ostart, ostart + (int64_t)nb * Q);
+  tile_store(a.out, so, ostart, ostart + (int64_t)nb * Q, a.out_words);
 }
 
 // ------------------------------------------------- TMA-bulk pipelined kernel
@@ -613,6 +653,10 @@ __global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? 3 : 2))) eq_tma_k
     const int64_t nb = (a.nblocks - tile0) < T ? (a.nblocks - tile0) : T;
     const TileWin wx = tile_window(a.x_bit0 + tile0 * B, nb * B);
     const TileWin wy = tile_window(a.y_bit0 + tile0 * B, nb * B);
+    BX_CHECK((int64_t)wx.bytes / 4 - 1, sw, 5);
+    BX_CHECK((int64_t)wy.bytes / 4 - 1, sw, 5);
+    BX_CHECK((wx.lo + wx.bytes) / 4 - 1, a.x_limit, 6);
+    BX_CHECK((wy.lo + wy.bytes) / 4 - 1, a.y_limit, 6);
     mbar_expect_tx(&bars[st], wx.bytes + wy.bytes);
     bulk_g2s(bufs + (2 * st) * sw, xg + wx.lo, wx.bytes, &bars[st]);
     bulk_g2s(bufs + (2 * st + 1) * sw, yg + wy.lo, wy.bytes, &bars[st]);
@@ -642,9 +686,9 @@ __global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? 3 : 2))) eq_tma_k
     phase[st] ^= 1u;
     __syncthreads();
     tile_compute<Q>(a, bufs + (2 * st) * sw, bufs + (2 * st + 1) * sw, wx.bit0, wy.bit0, so,
-                    ostart & 31, nb);
+                    ostart & 31, nb, sw, sw, ow_max);
     __syncthreads();
-    tile_store(a.out, so, ostart, ostart + (int64_t)nb * Q);
+    tile_store(a.out, so, ostart, ostart + (int64_t)nb * Q, a.out_words);
   }
 }
 
@@ -662,6 +706,9 @@ struct DirectArgs {
   int64_t nblocks;
   uint32_t* out;       // word holding output bit 0 of block 0
   int units;           // 128-bit units per block (q*n/128)
+  int64_t x_limit;     // readable 16-byte units from x / y (checked builds)
+  int64_t y_limit;
+  int64_t out_words;   // writable words from out (checked builds)
 };
 
 template <int Q>
@@ -719,6 +766,8 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const 
   if (l < a.nblocks) {
     const uint4* xp = a.x + l * a.units;
     const uint4* yp = a.y + l * a.units;
+    BX_CHECK((l + 1) * (U > 0 ? U : a.units) - 1, a.x_limit, 7);
+    BX_CHECK((l + 1) * (U > 0 ? U : a.units) - 1, a.y_limit, 7);
     Wide<CW> c;
     // U > 0: the unit count is a compile-time constant (fully unrolled,
     // all loads issued up front); U == 0: runtime count.
@@ -765,6 +814,7 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const 
     if ((lane % G) == 0 && first < a.nblocks) {
       const int64_t w = first * Q / 32;
       const int64_t valid = (a.nblocks - first) * Q;
+      BX_CHECK(w, a.out_words, 8);
       if (valid >= 32) {
         a.out[w] = v;
       } else {
@@ -776,7 +826,10 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const 
   } else {
     if (l < a.nblocks) {
 #pragma unroll
-      for (int i = 0; i < EW; i++) a.out[l * EW + i] = z.w[i];
+      for (int i = 0; i < EW; i++) {
+        BX_CHECK(l * EW + i, a.out_words, 8);
+        a.out[l * EW + i] = z.w[i];
+      }
     }
   }
 }

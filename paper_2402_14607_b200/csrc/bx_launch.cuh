@@ -160,6 +160,9 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
       d.nblocks = a.nblocks;
       d.out = a.out + a.out_bit0 / 32;
       d.units = c.units;
+      d.x_limit = a.x_limit / 4 - a.x_bit0 / 128;
+      d.y_limit = a.y_limit / 4 - a.y_bit0 / 128;
+      d.out_words = a.out_words - a.out_bit0 / 32;
       const dim3 g((unsigned)c.grid), b(c.threads);
       switch (c.units) {
         case 1: eq_direct_kernel<Q, 1><<<g, b, 0, s>>>(d); break;

@@ -46,6 +46,18 @@ t = np.random.default_rng(1).random((16, 16))
 cum = np.cumsum(t / t.sum(1, keepdims=True), axis=1)
 cum[:, -1] = 1.0
 D.markov_chain(u, torch.from_numpy(cum).cuda(), 4, 3)
+# neq with growing widths and random run shapes on the TMA / staged / direct paths
+for _ in range(40):
+    q = rnd.randint(1, 128)
+    n = rnd.randint(1, 90)
+    k = rnd.randint(1, 600)
+    xo, yo, oo = rnd.randint(0, 200), rnd.randint(0, 200), rnd.randint(0, 70)
+    nb = (max(xo, yo) + k * q * n + 7) // 8
+    xb, yb = rnd.randbytes(nb), rnd.randbytes(nb)
+    xd, xn = D.to_device_stream(xb, "cuda")
+    yd, yn = D.to_device_stream(yb, "cuda")
+    D.extract_eq(xd, xn, yd, yn, q, n, k, x_bit0=xo, y_bit0=yo, out_bit0=oo)
 torch.cuda.synchronize()
-print("fails", fails)
-sys.exit(1 if fails else 0)
+viol, first = _lib.checked_violations()
+print("fails", fails, "checked_violations", viol, "first", first)
+sys.exit(1 if fails or viol > 0 else 0)
