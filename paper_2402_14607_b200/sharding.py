@@ -15,6 +15,7 @@ Two entry points:
 """
 from __future__ import annotations
 
+import os
 import threading
 
 import numpy as np
@@ -84,7 +85,7 @@ class _Stager:
     stream; a slot is reused only after its previous H2D completed (event)."""
 
     SLOTS = 4
-    THREADS = 8
+    THREADS = int(os.environ.get("BX_STAGE_THREADS", "8"))
 
     def __init__(self, slot_bytes: int):
         import concurrent.futures as cf
@@ -157,7 +158,7 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
             # threads (see _Stager) so their H2D is asynchronous too
             cx = torch.cuda.Stream(dev)
             cy = torch.cuda.Stream(dev)
-            stager = None if pinned else _Stager(PIPE_CHUNK_BYTES // 2)
+            stager = None if pinned else _Stager(int(os.environ.get("BX_STAGE_MB", "32")) << 20)
             step = max(ALIGN_BLOCKS, (PIPE_CHUNK_BYTES * 8 // B) // ALIGN_BLOCKS * ALIGN_BLOCKS)
             if stager is not None:
                 step = max(ALIGN_BLOCKS, (stager.slot_bytes * 8 // B - 16) // ALIGN_BLOCKS * ALIGN_BLOCKS)
