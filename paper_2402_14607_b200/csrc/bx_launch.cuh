@@ -92,13 +92,17 @@ inline LaunchCfg choose_direct(int q, int n, int64_t nblocks) {
 // Persistent TMA-bulk variant of a staged configuration: two stages of both
 // windows (16-byte padded) plus two output tiles; grid = resident CTAs.
 inline int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
+  // per device (the library may drive several GPUs from one process)
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int v = 148;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
+    cache[dev] = v;
+  }
+  return cache[dev];
 }
 
 // Shared memory per TMA CTA: two stages of both windows; kept small enough for
