@@ -15,10 +15,11 @@
 // formulations are used, chosen at compile time by Q:
 //
 //  * Diag (Q <= 8): a 32-bit chunk holds E = 32/Q elements.  For every shift
-//    d in (-Q, Q):  acc_d ^= (X >> d) & Y   (X << -d for d < 0).  Bit jQ+b of
-//    acc_d accumulates x_{j,b+d} * y_{j,b}; at the end
-//        c_k = XOR_{b} parity(acc_{k-2b} & M_b),   M_b = {jQ+b : j < E}.
-//    Cost: 2Q-1 LOP3 + 2Q-2 shifts per chunk of E elements (ALU + IMAD.SHL).
+//    d in [0, Q): pos_d ^= X & (Y << d), and for d in [1, Q):
+//    neg_d ^= (X << d) & Y.  Each accumulator bit holds x_{j,a} * y_{j,b} for
+//    one (a, b) with a - b = +-d; at the end
+//        c_k = parity(XOR_{a+b=k} acc_{a-b} & M),   M = that pair's positions.
+//    Cost: 2Q-1 LOP3 (ALU) + 2Q-2 left shifts (IMAD.SHL, FMA pipe) per chunk.
 //
 //  * Holes (Q >= 9): elements are cut into 16-bit halves; a 16x16 carry-less
 //    product is formed with nine 32-bit IMADs on "holed" operands
@@ -436,7 +437,8 @@ __device__ __forceinline__ void read_elem(const uint32_t* src, int64_t off, int6
 // Blocks [tile0, tile0 + nb) of a tile: each group of tpb threads computes one
 // block from the word arrays sx / sy (shared or global memory) whose block 0
 // starts at bit xbase / ybase, and ORs its q-bit output into `so` at bit
-// obase + grp*Q (so must be zeroed).  Ends with the caller's __syncthreads.
+// obase + grp*Q (so must be zeroed).  xlim / ylim / olim are the word bounds of
+// sx / sy / so (checked builds).  Ends with the caller's __syncthreads.
 template <int Q>
 __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx, const uint32_t* sy,
                                              int64_t xbase, int64_t ybase, uint32_t* so,
