@@ -676,7 +676,13 @@ __global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? 3 : 2))) eq_tma_k
   int st = 0;
   for (; t < ntiles; t += gridDim.x, st ^= 1) {
     const int64_t tn = t + gridDim.x;
-    if (threadIdx.x == 0 && tn < ntiles) issue(tn, st ^ 1);
+    if (threadIdx.x == 0 && tn < ntiles) {
+      // the buffer being refilled was last read through the generic proxy
+      // (before the previous iteration's __syncthreads); order those reads
+      // before the async-proxy (TMA) writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tn, st ^ 1);
+    }
     const int64_t tile0 = t * T;
     const int nb = (int)((a.nblocks - tile0) < T ? (a.nblocks - tile0) : T);
     const int64_t ostart = a.out_bit0 + tile0 * Q;
