@@ -69,6 +69,21 @@ def parity_table(q: int) -> np.ndarray:
     return (p & np.uint32(1)).astype(np.uint8)
 
 
+_parity_table = parity_table   # reference-internal name (verify.py:252-259)
+
+
+def _window_table(ctx: GFContext, base: int, width: int) -> np.ndarray:
+    """W[d, u] = d * (u << base) mod modulus for all q-bit d and width-bit u
+    (reference-internal helper, verify.py:166-182): XOR of shift-table columns
+    per set bit of u."""
+    tabs = shift_tables(ctx)
+    us = np.arange(1 << width)
+    w = np.zeros((1 << ctx.q, 1 << width), dtype=np.uint32)
+    for j in range(width):
+        w[:, ((us >> j) & 1).astype(bool)] ^= tabs[base + j][:, None]
+    return w
+
+
 def walsh_transform(rows) -> np.ndarray:
     """out[..., a] = sum_w rows[..., w] * (-1)^popcount(a & w), exact int64."""
     a = np.array(rows, dtype=np.int64, copy=True)

@@ -16,7 +16,7 @@ import sys
 REPO = pathlib.Path(__file__).resolve().parents[1]
 SRC = pathlib.Path("/root/reference/pkg/tests")
 DST = REPO / "refcompat"
-MODULES = ["test_extractor.py", "test_gf2q.py", "test_bitio.py", "test_params.py"]
+MODULES = ["test_extractor.py", "test_gf2q.py", "test_bitio.py", "test_params.py", "test_verify.py"]
 
 
 def prepare() -> None:
