@@ -94,6 +94,27 @@ int bx_launch_info(int q, int n, int64_t nblocks, int* tpb, int* tile, int* stag
 int bx_pack(const void* samples, int elem_bytes, int b, int64_t count,
             void* out, int64_t out_bit0, void* stream);
 
+/* ---- native streaming pipeline ----------------- */
+
+/*
+ * Push-based equal-width extraction for producers outside Python.  Each push
+ * hands over the next nbytes (<= chunk_bytes) of both streams from host
+ * memory; every block completed by the bytes so far is extracted on `device`
+ * and the packed output's whole bytes are written to out (capacity out_cap),
+ * *out_bytes = count.  Partial blocks and the last partial output byte carry
+ * over, so the concatenated outputs of any push sequence (plus flush) equal
+ * one run over the concatenated streams.  Synchronous per push.
+ */
+typedef struct bx_pipe bx_pipe;
+bx_pipe* bx_pipe_create(int q, int n, int64_t chunk_bytes, int device);
+int bx_pipe_push(bx_pipe* p, const void* x, const void* y, int64_t nbytes, void* out,
+                 int64_t out_cap, int64_t* out_bytes);
+/* Emits the carried partial output byte (zero padded), if any. */
+int bx_pipe_flush(bx_pipe* p, void* out, int64_t* out_bytes);
+/* Blocks extracted so far (or -1 for NULL). */
+int64_t bx_pipe_blocks(const bx_pipe* p);
+void bx_pipe_destroy(bx_pipe* p);
+
 /* ---- device source simulators ---------------- */
 
 /*

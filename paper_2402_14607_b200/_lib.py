@@ -32,6 +32,11 @@ SIGNATURES = {
     "bx_pack": (_i32, [_vp, _i32, _i32, _i64, _vp, _i64, _vp]),
     "bx_launch_count": (_i64, [_i32]),
     "bx_checked_violations": (_i64, [_i32, _PI64]),
+    "bx_pipe_create": (_vp, [_i32, _i32, _i64, _i32]),
+    "bx_pipe_push": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _PI64]),
+    "bx_pipe_flush": (_i32, [_vp, _vp, _PI64]),
+    "bx_pipe_blocks": (_i64, [_vp]),
+    "bx_pipe_destroy": (None, [_vp]),
     "bx_bernoulli_bits": (_i32, [_vp, _i64, ctypes.c_double, ctypes.c_uint64, _i64, _vp]),
     "bx_xor_scan_scratch_bytes": (_i64, [_i64, _i32]),
     "bx_xor_scan_rows": (_i32, [_vp, _i64, _i32, _vp, _vp]),

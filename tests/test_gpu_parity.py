@@ -274,3 +274,23 @@ def test_lazy_iteration_matches_run():
     bx.extract_eq(xb, yb, plan).run(sink)
     assert acc.to_bytes(len(sink.getvalue()), "little") == sink.getvalue()
     assert sink.getvalue() == coracle.extract_eq(xb, yb, q, n, k)
+
+
+def test_native_pipe_random_push_sizes():
+    """bx_pipe: any sequence of push sizes equals one run over the concatenation."""
+    from paper_2402_14607_b200.pipe import Pipe
+    rnd = random.Random(17)
+    for q, n in [(4, 64), (13, 7), (56, 48), (128, 8), (1, 3), (80, 71)]:
+        total = rnd.randint(20_000, 120_000)
+        xb, yb = rnd.randbytes(total), rnd.randbytes(total)
+        out = []
+        with Pipe(q, n, chunk_bytes=9000) as p:
+            pos = 0
+            while pos < total:
+                step = min(total - pos, rnd.choice([1, 7, 100, 4096, 9000]))
+                out.append(p.push(xb[pos:pos + step], yb[pos:pos + step]))
+                pos += step
+            out.append(p.flush())
+            k = p.blocks
+        assert k == total * 8 // (q * n)
+        assert b"".join(out) == coracle.extract_eq(xb, yb, q, n, k), (q, n)
