@@ -94,6 +94,16 @@ int bx_launch_info(int q, int n, int64_t nblocks, int* tpb, int* tile, int* stag
 int bx_pack(const void* samples, int elem_bytes, int b, int64_t count,
             void* out, int64_t out_bit0, void* stream);
 
+/*
+ * Inner products over GF(2^q) with a caller-chosen modulus (GFContext(q,
+ * modulus), reference gf2q.py:99-183): out[v] = sum_j x[v][j] * y[v][j] for
+ * nvec vectors of n elements.  Elements, the modulus's low part (modulus minus
+ * x^q) and outputs are 128-bit little-endian (4 uint32 words each), device
+ * memory.  A simple per-vector kernel for API calls, not the extraction path.
+ */
+int bx_gf_ip_generic(int q, const void* modulus_low, const void* x, const void* y, int n,
+                     int64_t nvec, void* out, void* stream);
+
 /* ---- native streaming pipeline ----------------- */
 
 /*

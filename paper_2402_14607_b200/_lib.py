@@ -32,6 +32,7 @@ SIGNATURES = {
     "bx_pack": (_i32, [_vp, _i32, _i32, _i64, _vp, _i64, _vp]),
     "bx_launch_count": (_i64, [_i32]),
     "bx_checked_violations": (_i64, [_i32, _PI64]),
+    "bx_gf_ip_generic": (_i32, [_i32, _vp, _vp, _vp, _i32, _i64, _vp, _vp]),
     "bx_pipe_create": (_vp, [_i32, _i32, _i64, _i32]),
     "bx_pipe_push": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _PI64]),
     "bx_pipe_flush": (_i32, [_vp, _vp, _PI64]),

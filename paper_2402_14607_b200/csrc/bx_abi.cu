@@ -23,6 +23,8 @@ cudaError_t launch_ip_table(int, uint32_t, int, uint32_t, uint32_t, uint16_t*, c
 cudaError_t launch_ip_hist(int, uint32_t, int, uint32_t, uint32_t, uint32_t*, cudaStream_t);
 cudaError_t launch_rows_uniform(const uint32_t*, uint32_t, uint32_t, uint32_t, uint8_t*,
                                 cudaStream_t);
+cudaError_t launch_gf_ip_generic(int, const uint32_t*, const uint32_t*, const uint32_t*, int, int64_t,
+                                 uint32_t*, cudaStream_t);
 
 #define BX_EXTERN_Q(Q) extern template cudaError_t launch_eq<Q>(const EqArgs&, const LaunchCfg&, cudaStream_t);
 #define BX_X8(b) BX_EXTERN_Q(b + 1) BX_EXTERN_Q(b + 2) BX_EXTERN_Q(b + 3) BX_EXTERN_Q(b + 4) \
@@ -301,6 +303,22 @@ int bx_rows_uniform(const void* counts, uint32_t nrows, uint32_t bins, uint32_t 
   cudaError_t e = bx::launch_rows_uniform(static_cast<const uint32_t*>(counts), nrows, bins, expected,
                                           static_cast<uint8_t*>(flags), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_rows_uniform: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int bx_gf_ip_generic(int q, const void* modulus_low, const void* x, const void* y, int n,
+                     int64_t nvec, void* out, void* stream) {
+  if (q < 1 || q > 128) return fail(BX_ERANGE, "field width outside 1..128");
+  if (n < 1 || nvec < 0) return fail(BX_EINVAL, "n must be >= 1 and nvec >= 0");
+  if (nvec == 0) return BX_OK;
+  if (!modulus_low || !x || !y || !out) return fail(BX_EINVAL, "null buffer");
+  const DeviceScope scope(out);
+  cudaError_t e = bx::launch_gf_ip_generic(q, static_cast<const uint32_t*>(modulus_low),
+                                           static_cast<const uint32_t*>(x), static_cast<const uint32_t*>(y),
+                                           n, nvec, static_cast<uint32_t*>(out),
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_gf_ip_generic: ") + cudaGetErrorString(e));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return BX_OK;
 }

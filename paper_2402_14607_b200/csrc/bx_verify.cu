@@ -120,3 +120,58 @@ cudaError_t launch_rows_uniform(const uint32_t* counts, uint32_t nrows, uint32_t
 }
 
 }  // namespace bx
+
+// ---------------------------------------------------------------------------
+// Runtime-modulus inner products (GFContext with a caller-chosen irreducible
+// modulus; reference gf2q.py:99-183 allows any).  Not a hot path: one thread
+// per vector, shift-and-XOR carry-less products over 4-word (128-bit)
+// operands accumulated unreduced, one bit-serial reduction by the modulus.
+namespace bx {
+
+__device__ __forceinline__ void shl_xor8(uint32_t (&c)[8], const uint32_t (&b)[4], int s) {
+  const int ws = s >> 5, bs = s & 31;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const uint32_t v = b[i];
+    if (ws + i < 8) c[ws + i] ^= v << bs;
+    if (bs && ws + i + 1 < 8) c[ws + i + 1] ^= v >> (32 - bs);
+  }
+}
+
+__global__ void gf_ip_generic_kernel(int q, const uint32_t* modulus, const uint32_t* x,
+                                     const uint32_t* y, int n, int64_t nvec, uint32_t* out) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvec) return;
+  uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int j = 0; j < n; j++) {
+    const uint32_t* a = x + (v * n + j) * 4;
+    uint32_t b[4] = {y[(v * n + j) * 4], y[(v * n + j) * 4 + 1], y[(v * n + j) * 4 + 2],
+                     y[(v * n + j) * 4 + 3]};
+    for (int i = 0; i < q; i++)
+      if ((a[i >> 5] >> (i & 31)) & 1u) shl_xor8(c, b, i);
+  }
+  // reduce: for every set bit i >= q (top down) XOR modulus << (i - q)
+  uint32_t m[4] = {modulus[0], modulus[1], modulus[2], modulus[3]};  // full modulus minus x^q
+  for (int i = 2 * q - 2; i >= q; i--) {
+    if ((c[i >> 5] >> (i & 31)) & 1u) {
+      c[i >> 5] ^= 1u << (i & 31);
+      shl_xor8(c, m, i - q);
+    }
+  }
+  for (int w = 0; w < 4; w++) {
+    const int lo = 32 * w;
+    uint32_t val = c[w];
+    if (lo >= q) val = 0;
+    else if (q - lo < 32) val &= (1u << (q - lo)) - 1u;
+    out[v * 4 + w] = val;
+  }
+}
+
+cudaError_t launch_gf_ip_generic(int q, const uint32_t* modulus, const uint32_t* x, const uint32_t* y,
+                                 int n, int64_t nvec, uint32_t* out, cudaStream_t st) {
+  if (nvec <= 0) return cudaSuccess;
+  gf_ip_generic_kernel<<<(unsigned)((nvec + 127) / 128), 128, 0, st>>>(q, modulus, x, y, n, nvec, out);
+  return cudaGetLastError();
+}
+
+}  // namespace bx

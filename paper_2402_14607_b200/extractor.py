@@ -88,16 +88,49 @@ def _pack_vectors(vectors: Sequence[Sequence[int]], q: int) -> bytes:
     return acc.to_bytes((pos + 7) // 8, "little")
 
 
+def _generic_inner_products(q: int, modulus: int, xs, ys, dev) -> list[int]:
+    """Inner products under a caller-chosen modulus (bx_gf_ip_generic)."""
+    import torch
+
+    from . import _lib
+    from . import device as D
+
+    out = [0] * len(xs)
+    groups: dict[int, list[int]] = {}
+    for i, v in enumerate(xs):
+        groups.setdefault(len(v), []).append(i)
+    low = (modulus ^ (1 << q)).to_bytes(16, "little")
+    mod_d = torch.frombuffer(bytearray(low), dtype=torch.uint8).to(dev)
+    for n, idx in groups.items():
+        xb = b"".join(int(v).to_bytes(16, "little") for i in idx for v in xs[i])
+        yb = b"".join(int(v).to_bytes(16, "little") for i in idx for v in ys[i])
+        xd = torch.frombuffer(bytearray(xb), dtype=torch.uint8).to(dev)
+        yd = torch.frombuffer(bytearray(yb), dtype=torch.uint8).to(dev)
+        res = torch.empty(16 * len(idx), dtype=torch.uint8, device=dev)
+        with torch.cuda.device(dev):
+            _lib.check(_lib.lib().bx_gf_ip_generic(q, mod_d.data_ptr(), xd.data_ptr(), yd.data_ptr(), n,
+                                                   len(idx), res.data_ptr(), D.stream_ptr(None, dev)),
+                       "bx_gf_ip_generic")
+        host = res.cpu().numpy().tobytes()
+        for k, i in enumerate(idx):
+            out[i] = int.from_bytes(host[16 * k:16 * k + 16], "little")
+    return out
+
+
 def _device_inner_products(q: int, xs: Sequence[Sequence[int]], ys: Sequence[Sequence[int]],
-                           device=None) -> list[int]:
+                           device=None, modulus: int | None = None) -> list[int]:
     """sum_j x_j * y_j over GF(2^q) for each vector pair, on the GPU.
 
     Vectors are grouped by length; each group is one bx_extract_eq launch with
-    one block per pair.  Elements must already be validated.
+    one block per pair (default modulus), or one bx_gf_ip_generic launch for a
+    caller-chosen modulus.  Elements must already be validated.
     """
     from . import device as D
+    from .gf2q import modulus_int
 
     dev = D.require_cuda(device)
+    if modulus is not None and modulus != modulus_int(q):
+        return _generic_inner_products(q, modulus, xs, ys, dev)
     out = [0] * len(xs)
     groups: dict[int, list[int]] = {}
     for i, v in enumerate(xs):
@@ -127,8 +160,7 @@ def ext_ip(ctx: GFContext, x: Sequence[int], y: Sequence[int]) -> int:
         ctx.check(v)
     for v in y:
         ctx.check(v)
-    ctx._device_ok()
-    return _device_inner_products(ctx.q, [tuple(x)], [tuple(y)])[0]
+    return _device_inner_products(ctx.q, [tuple(x)], [tuple(y)], modulus=ctx.modulus)[0]
 
 
 def run_parallel(blocks: Iterable[BlockPair], workers: int, *,
@@ -166,17 +198,17 @@ def run_parallel(blocks: Iterable[BlockPair], workers: int, *,
                     pair.ctx.check(v)
                 for v in pair.y:
                     pair.ctx.check(v)
-                pair.ctx._device_ok()
             except Exception as exc:  # noqa: BLE001 - re-raised in order below
                 bad_at, bad_exc = k, exc
                 break
         good = batch if bad_at is None else batch[:bad_at]
         results = [0] * len(good)
-        by_q: dict[int, list[int]] = {}
+        by_field: dict[tuple[int, int], list[int]] = {}
         for k, pair in enumerate(good):
-            by_q.setdefault(pair.ctx.q, []).append(k)
-        for q, ks in by_q.items():
-            vals = _device_inner_products(q, [good[k].x for k in ks], [good[k].y for k in ks])
+            by_field.setdefault((pair.ctx.q, pair.ctx.modulus), []).append(k)
+        for (q, mod), ks in by_field.items():
+            vals = _device_inner_products(q, [good[k].x for k in ks], [good[k].y for k in ks],
+                                          modulus=mod)
             for k, v in zip(ks, vals):
                 results[k] = v
         for pair, v in zip(good, results):

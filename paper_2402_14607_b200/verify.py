@@ -125,7 +125,7 @@ def _feasible(ctx: GFContext, n: int, cap: int, what: str) -> int:
 
 def _default_modulus(ctx: GFContext) -> None:
     if not ctx._default:
-        raise NotImplementedError("device kernels implement the shipped default modulus only")
+        raise NotImplementedError("the exhaustive verification kernels use the shipped default modulus")
 
 
 # ---------------------------------------------------------- device tables

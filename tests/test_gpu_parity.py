@@ -294,3 +294,38 @@ def test_native_pipe_random_push_sizes():
             k = p.blocks
         assert k == total * 8 // (q * n)
         assert b"".join(out) == coracle.extract_eq(xb, yb, q, n, k), (q, n)
+
+
+def test_custom_modulus_contexts():
+    """GFContext with a non-default irreducible modulus multiplies on the GPU."""
+    from oracle import pyoracle
+    rnd = random.Random(41)
+
+    def other_modulus(q):
+        # an irreducible modulus different from the shipped one (scan from the top)
+        default = bx.modulus_int(q)
+        for k in range(q - 1, 0, -1):
+            m = (1 << q) | (1 << k) | 1
+            if m != default and bx.is_irreducible(m):
+                return m
+        for a_ in range(q - 1, 3, -1):
+            for b_ in range(a_ - 1, 1, -1):
+                m = (1 << q) | (1 << a_) | (1 << b_) | 0b11
+                if m != default and bx.is_irreducible(m):
+                    return m
+        return None
+
+    for q in (3, 8, 13, 64, 100, 127):
+        mod = other_modulus(q)
+        assert mod is not None
+        ctx = bx.GFContext(q, modulus=mod)
+        a = [rnd.getrandbits(q) for _ in range(20)]
+        b = [rnd.getrandbits(q) for _ in range(20)]
+        want = [pyoracle.gf_mul(q, mod, x, y) for x, y in zip(a, b)]
+        assert ctx.mul_many(a, b) == want, q
+        assert ctx.mul(a[0], b[0]) == want[0]
+        xs, ys = a[:7], b[:7]
+        ip = 0
+        for x, y in zip(xs, ys):
+            ip ^= pyoracle.gf_mul(q, mod, x, y)
+        assert bx.ext_ip(ctx, xs, ys) == ip
