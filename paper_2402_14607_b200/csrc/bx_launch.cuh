@@ -75,17 +75,22 @@ inline LaunchCfg choose_launch(int q, int n, int64_t nblocks) {
   return c;
 }
 
+inline int sm_count();
+
 inline LaunchCfg choose_direct(int q, int n, int64_t nblocks) {
   LaunchCfg c;
   c.family = q <= kDiagMaxQ ? 0 : 1;
   c.direct = 1;
   c.tpb_log2 = 0;
-  c.tile = 256;
-  c.threads = 256;
+  // small runs: narrower CTAs so the blocks spread over more SMs
+  int threads = 256;
+  while (threads > 64 && (nblocks + threads - 1) / threads < 2 * (int64_t)sm_count()) threads /= 2;
+  c.tile = threads;
+  c.threads = threads;
   c.staged = 0;
   c.smem = 0;
   c.units = (int)((int64_t)q * n / 128);
-  c.grid = (nblocks + 255) / 256;
+  c.grid = (nblocks + threads - 1) / threads;
   return c;
 }
 
