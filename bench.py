@@ -325,8 +325,14 @@ def run_ours(args, wl) -> None:
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "kernel_ms": ms_step, "launch": _lib.launch_info(wl.q, wl.n, nblocks)}
     li = roofline["launch"]
-    roofline["kernel"] = (f"bx::eq_direct_kernel<{wl.q}, {wl.block_bits // 128}>" if li["direct"]
+    roofline["kernel"] = (f"bx::eq_direct_kernel<{wl.q}, {u if (u := wl.block_bits // 128) in (1, 2, 4, 8) else 0}>"
+                          if li["direct"]
+                          else f"bx::eq_tma_kernel<{wl.q}>" if li["tma"]
                           else f"bx::eq_kernel<{wl.q}, {'true' if li['staged'] else 'false'}>")
+    if not hbm_bound:
+        roofline["int_note"] = ("work counted as schoolbook n*q^2 AND-XOR pairs; the q>=9 kernels "
+                                "multiply 16-bit halves with Karatsuba (27 instead of 64 half "
+                                "products at q=128), so frac can exceed 1")
 
     # ---- e2e: public API from host memory, every step H2D + kernels + D2H.  The
     # optional legs below record an error string instead of killing the line;
