@@ -15,11 +15,13 @@
 // formulations are used, chosen at compile time by Q:
 //
 //  * Diag (Q <= 8): a 32-bit chunk holds E = 32/Q elements.  For every shift
-//    d in [0, Q): pos_d ^= X & (Y << d), and for d in [1, Q):
-//    neg_d ^= (X << d) & Y.  Each accumulator bit holds x_{j,a} * y_{j,b} for
-//    one (a, b) with a - b = +-d; at the end
-//        c_k = parity(XOR_{a+b=k} acc_{a-b} & M),   M = that pair's positions.
-//    Cost: 2Q-1 LOP3 (ALU) + 2Q-2 left shifts (IMAD.SHL, FMA pipe) per chunk.
+//    d in [0, Q): acc_d ^= (X & (Y << d)) ^ ((X << d) & Y).  Bit jQ+p of acc_d
+//    (p >= d) holds the two products x_{j,a} y_{j,b} with a + b = 2p - d and
+//    |a - b| = d; at the end
+//        c_k = XOR over elements and d of bit (k+d)/2 of acc_d,
+//    formed by a fold over elements and a bit spread (Q = 4, 8) or masked
+//    parities.  Cost: 2Q-1 LOP3 (ALU) + 2Q-2 left shifts (IMAD.SHL, FMA pipe)
+//    per chunk.
 //
 //  * Holes (Q >= 9): elements are cut into 16-bit halves; a 16x16 carry-less
 //    product is formed with nine 32-bit IMADs on "holed" operands
@@ -188,10 +190,15 @@ template <int Q>
 struct Diag {
   static constexpr int E = 32 / Q;   // elements per 32-bit chunk
   static constexpr int EB = E * Q;   // bits per chunk
-  // pos[d] (d >= 0) accumulates X & (Y << d): bit jQ+b+d holds x_{j,b+d} y_{j,b}.
-  // neg[d] (d >= 1) accumulates (X << d) & Y: bit jQ+b holds x_{j,b-d} y_{j,b}.
-  // Only left shifts, so the compiler issues them as IMAD.SHL on the FMA pipe
-  // and the ALU pipe carries just the 2Q-1 LOP3s per chunk.
+  // acc(d) is the sum of the two diagonals at distance d:
+  //   X & (Y << d)   bit jQ+p holds x_{j,p}   y_{j,p-d}
+  //   (X << d) & Y   bit jQ+p holds x_{j,p-d} y_{j,p}
+  // both valid for p >= d and both contributing to c_{2p-d}, so they share one
+  // register.  Only left shifts, so the compiler issues them as IMAD.SHL on the
+  // FMA pipe and the ALU pipe carries just the 2Q-1 LOP3s per chunk.
+  // The two diagonals are kept in separate registers during the block (pos,
+  // neg: one a ^ (b & c) LOP3 each; a merged register makes the compiler
+  // build (X & Y<<d) ^ (X<<d & Y) trees, +25% LOP3) and merged at the end.
   uint32_t pos[Q];
   uint32_t neg[Q];
 
@@ -207,31 +214,64 @@ struct Diag {
     for (int d = 1; d < Q; d++) neg[d] ^= (X << d) & Y;
   }
 
-  static __host__ __device__ constexpr uint32_t mask_b(int b) {
+  __device__ __forceinline__ uint32_t acc(int d) const { return d ? pos[d] ^ neg[d] : pos[0]; }
+
+  static __host__ __device__ constexpr uint32_t mask_b(int b) {   // bit b of every element
     uint32_t m = 0;
     for (int j = 0; j < E; j++) m |= 1u << (j * Q + b);
     return m;
   }
+  static __host__ __device__ constexpr uint32_t mask_ge(int d) {  // bits >= d of every element
+    uint32_t m = 0;
+    for (int b = d; b < Q; b++) m |= mask_b(b);
+    return m;
+  }
 
-  // unreduced c (2Q-1 <= 15 bits): c_k = parity(XOR_b acc_{k-2b} & M_b), one
-  // LOP3 per (k, b) pair and one POPC per k.  For d >= 0 the product
-  // x_{j,a} y_{j,b} (a = b + d) sits at bit jQ+a of pos[d], i.e. under M_a.
+  // unreduced c (2Q-1 <= 15 bits), c_k = XOR over elements and d of the valid
+  // bits p = (k+d)/2 of acc[d].
   __device__ __forceinline__ uint32_t unreduced() const {
-    uint32_t c = 0;
+    if constexpr (Q == 4 || Q == 8) {
+      // Fold/spread form (~28 ops at Q=8 instead of ~Q^2 LOP3 + 2Q-1 POPC):
+      // for d = 2e (2e+1) the valid bits shifted down by e go to A (B); bit p'
+      // of the element-fold of A (B) then belongs at c_{2p'} (c_{2p'-1}), so
+      // c = spread(fold A) ^ (spread(fold B) >> 1), spread: bit p -> bit 2p.
+      // The right shift by e <= d only pulls in masked (zero) bits.
+      uint32_t A = 0u, B = 0u;
 #pragma unroll
-    for (int k = 0; k < 2 * Q - 1; k++) {
-      uint32_t t = 0;
-#pragma unroll
-      for (int b = 0; b < Q; b++) {
-        const int a = k - b;
-        if (a < 0 || a >= Q) continue;
-        const int d = a - b;
-        if (d >= 0) t ^= pos[d] & mask_b(a);
-        else t ^= neg[-d] & mask_b(b);
+      for (int d = 0; d < Q; d++) {
+        const uint32_t t = (acc(d) >> (d >> 1)) & (mask_ge(d) >> (d >> 1));
+        if (d & 1) B ^= t;
+        else A ^= t;
       }
-      c |= (uint32_t)(__popc(t) & 1) << k;
+      A ^= A >> 16;                                  // 2 elements per 16-bit lane left
+      B ^= B >> 16;
+      uint32_t v = __byte_perm(A, B, 0x5410);        // A lane in bits 0-15, B lane in 16-31
+      constexpr uint32_t lane = (1u << Q) - 1u;
+#pragma unroll
+      for (int s = 8; s > Q; s >>= 1) v ^= v >> s;
+      v = (v ^ (v >> Q)) & (lane | (lane << 16));    // each lane: Q-bit fold at its bit 0
+      if constexpr (Q == 8) v = (v | (v << 4)) & 0x0F0F0F0Fu;
+      v = (v | (v << 2)) & 0x33333333u;
+      v = (v | (v << 1)) & 0x55555555u;
+      return (v & 0xFFFFu) ^ (v >> 17);
+    } else {
+      // c_k = parity(XOR_d acc[d] & M_{(k+d)/2}): one LOP3 per (k, d) pair and
+      // one POPC per k
+      uint32_t c = 0;
+#pragma unroll
+      for (int k = 0; k < 2 * Q - 1; k++) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int d = 0; d < Q; d++) {
+          if ((k + d) & 1) continue;
+          const int p = (k + d) >> 1;
+          if (p < d || p >= Q) continue;
+          t ^= acc(d) & mask_b(p);
+        }
+        c |= (uint32_t)(__popc(t) & 1) << k;
+      }
+      return c;
     }
-    return c;
   }
 };
 

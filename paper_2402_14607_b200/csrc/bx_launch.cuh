@@ -3,6 +3,8 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "bx_core.cuh"
@@ -121,6 +123,37 @@ inline size_t tma_budget() {
   return b;
 }
 
+// Occupancy of a TMA kernel configuration (setting its dynamic shared memory
+// limit first), memoised per (device, Q, threads, smem).
+inline cudaError_t tma_occupancy(const void* k, int q, int threads, size_t smem, int* occ) {
+  struct Entry {
+    int dev, q, threads;
+    size_t smem;
+    int occ;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> memo;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (const Entry& e : memo)
+      if (e.dev == dev && e.q == q && e.threads == threads && e.smem == smem) {
+        *occ = e.occ;
+        return cudaSuccess;
+      }
+  }
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, threads, smem);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  memo.push_back(Entry{dev, q, threads, smem, *occ});
+  return cudaSuccess;
+}
+
 inline void make_tma(LaunchCfg& c, int q, int n, int64_t nblocks) {
   const size_t kTmaBudget = tma_budget();
   const int64_t B = (int64_t)q * n;
@@ -147,13 +180,11 @@ template <int Q>
 cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
   if (c.tma) {
     auto k = eq_tma_kernel<Q>;
-    if (c.smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-      if (e != cudaSuccess) return e;
-    }
-    // persistent: exactly the CTAs that can be resident at once
+    // persistent: exactly the CTAs that can be resident at once.  The
+    // attribute and occupancy queries cost microseconds; they are cached per
+    // (device, threads, smem) so small launches stay launch-latency bound.
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c.threads, c.smem);
+    cudaError_t e = tma_occupancy(reinterpret_cast<const void*>(k), Q, c.threads, c.smem, &occ);
     if (e != cudaSuccess) return e;
     const int64_t ntiles = (a.nblocks + c.tile - 1) / c.tile;
     const int64_t resident = (int64_t)sm_count() * (occ > 0 ? occ : 1);

@@ -70,10 +70,13 @@ def extract_eq(x: torch.Tensor, x_bytes: int, y: torch.Tensor, y_bytes: int, q: 
     for t in (x, y, out):
         if not t.is_cuda or t.dtype != torch.uint8 or not t.is_contiguous():
             raise ValueError("device buffers must be contiguous uint8 CUDA tensors")
-    with torch.cuda.device(x.device):
-        _lib.check(_lib.lib().bx_extract_eq(
-            x.data_ptr(), x_bytes, x_bit0, y.data_ptr(), y_bytes, y_bit0, q, n, nblocks,
-            out.data_ptr(), out_bit0, stream_ptr(stream, x.device)), "bx_extract_eq")
+    # no torch.cuda.device() context: the library selects the device that owns
+    # x itself (DeviceScope in bx_abi.cu), which keeps small launches cheap
+    rc = _lib.lib().bx_extract_eq(x.data_ptr(), x_bytes, x_bit0, y.data_ptr(), y_bytes, y_bit0,
+                                  q, n, nblocks, out.data_ptr(), out_bit0,
+                                  stream_ptr(stream, x.device))
+    if rc:
+        _lib.check(rc, "bx_extract_eq")
     return out
 
 
