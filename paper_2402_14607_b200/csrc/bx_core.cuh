@@ -754,6 +754,7 @@ struct DirectArgs {
   int64_t nblocks;
   uint32_t* out;       // word holding output bit 0 of block 0
   int units;           // 128-bit units per block (q*n/128)
+  int wide;            // 1: x, y 32-byte aligned and units even -> 256-bit loads
   int64_t x_limit;     // readable 16-byte units from x / y (checked builds)
   int64_t y_limit;
   int64_t out_words;   // writable words from out (checked builds)
@@ -804,6 +805,51 @@ __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void
   }
 }
 
+// Two consecutive 128-bit units with one 256-bit load (LDG.E.ENL2.256 on
+// sm_100a): a whole 32-byte sector per thread per instruction.  Threads of a
+// warp read windows q*n/8 bytes apart, so every load touches 32 lines; at
+// q = 16 the 128-bit-load kernel is L1-throughput bound and the 256-bit loads
+// halve its L1 requests (+8%, profiles/r01_direct_sweep.txt).
+__device__ __forceinline__ void ldg256(const uint4* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
+// Unreduced inner product of one block's windows with 256-bit loads (units
+// even, xp / yp 32-byte aligned).
+template <int Q>
+__device__ __forceinline__ Wide<cdiv(2 * Q - 1, 32)> direct_block_wide(const uint4* xp, const uint4* yp,
+                                                                       int units) {
+  Wide<cdiv(2 * Q - 1, 32)> c;
+  if constexpr (Q <= kDiagMaxQ) {
+    Diag<Q> acc;
+    acc.init();
+#pragma unroll 2
+    for (int u = 0; u < units; u += 2) {
+      uint4 X0, X1, Y0, Y1;
+      ldg256(xp + u, X0, X1);
+      ldg256(yp + u, Y0, Y1);
+      direct_unit<Q>(X0, Y0, &acc);
+      direct_unit<Q>(X1, Y1, &acc);
+    }
+    c.w[0] = acc.unreduced();
+  } else {
+    Holes<Q> acc;
+    acc.init();
+#pragma unroll 1
+    for (int u = 0; u < units; u += 2) {
+      uint4 X0, X1, Y0, Y1;
+      ldg256(xp + u, X0, X1);
+      ldg256(yp + u, Y0, Y1);
+      direct_unit<Q>(X0, Y0, &acc);
+      direct_unit<Q>(X1, Y1, &acc);
+    }
+    c = acc.unreduced();
+  }
+  return c;
+}
+
 template <int Q, int U>
 __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
@@ -816,41 +862,45 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const 
     const uint4* yp = a.y + l * a.units;
     BX_CHECK((l + 1) * (U > 0 ? U : a.units) - 1, a.x_limit, 7);
     BX_CHECK((l + 1) * (U > 0 ? U : a.units) - 1, a.y_limit, 7);
-    Wide<CW> c;
     // U > 0: the unit count is a compile-time constant (fully unrolled,
     // all loads issued up front); U == 0: runtime count.
     const int units = U > 0 ? U : a.units;
-    if constexpr (Q <= kDiagMaxQ) {
-      Diag<Q> acc;
-      acc.init();
-#pragma unroll 4
-      for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
-      c.w[0] = acc.unreduced();
+    if (Q == 16 && a.wide) {
+      z = reduce<Q>(direct_block_wide<Q>(xp, yp, units));
     } else {
-      Holes<Q> acc;
-      acc.init();
-      if constexpr (Q == 128 && Holes<Q>::kPair) {
-        // one element per unit: pair consecutive units (elements)
-        int u = 0;
-#pragma unroll 1
-        for (; u + 1 < units; u += 2) {
-          const uint4 X0 = __ldg(xp + u), Y0 = __ldg(yp + u);
-          const uint4 X1 = __ldg(xp + u + 1), Y1 = __ldg(yp + u + 1);
-          const uint32_t a[4] = {X0.x, X0.y, X0.z, X0.w}, b[4] = {Y0.x, Y0.y, Y0.z, Y0.w};
-          const uint32_t c2[4] = {X1.x, X1.y, X1.z, X1.w}, d2[4] = {Y1.x, Y1.y, Y1.z, Y1.w};
-          acc.add2(a, b, c2, d2);
-        }
-        if (u < units) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
-      } else if constexpr (Q > 32) {
-#pragma unroll 1
+      Wide<CW> c;
+      if constexpr (Q <= kDiagMaxQ) {
+        Diag<Q> acc;
+        acc.init();
+#pragma unroll 4
         for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+        c.w[0] = acc.unreduced();
       } else {
+        Holes<Q> acc;
+        acc.init();
+        if constexpr (Q == 128 && Holes<Q>::kPair) {
+          // one element per unit: pair consecutive units (elements)
+          int u = 0;
+#pragma unroll 1
+          for (; u + 1 < units; u += 2) {
+            const uint4 X0 = __ldg(xp + u), Y0 = __ldg(yp + u);
+            const uint4 X1 = __ldg(xp + u + 1), Y1 = __ldg(yp + u + 1);
+            const uint32_t a[4] = {X0.x, X0.y, X0.z, X0.w}, b[4] = {Y0.x, Y0.y, Y0.z, Y0.w};
+            const uint32_t c2[4] = {X1.x, X1.y, X1.z, X1.w}, d2[4] = {Y1.x, Y1.y, Y1.z, Y1.w};
+            acc.add2(a, b, c2, d2);
+          }
+          if (u < units) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+        } else if constexpr (Q > 32) {
+#pragma unroll 1
+          for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+        } else {
 #pragma unroll 2
-        for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+          for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+        }
+        c = acc.unreduced();
       }
-      c = acc.unreduced();
+      z = reduce<Q>(c);
     }
-    z = reduce<Q>(c);
   }
   if constexpr (Q < 32) {
     // 32/Q consecutive blocks share one output word

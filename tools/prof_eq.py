@@ -13,6 +13,7 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 
 import torch
 
+from paper_2402_14607_b200 import _lib
 from paper_2402_14607_b200 import device as D
 from paper_2402_14607_b200 import workloads as W
 
@@ -46,7 +47,8 @@ def main():
     ms = e0.elapsed_time(e1) / a.launches
     gbs = nblocks * (2 * q * n / 8 + q / 8) / (ms * 1e-3) / 1e9
     print(f"q={q} n={n} blocks={nblocks}: {ms:.4f} ms/launch, {gbs:.1f} GB/s algorithmic, "
-          f"{2 * q * n * nblocks / (ms * 1e-3) / 1e9:.1f} Gbit/s raw in")
+          f"{2 * q * n * nblocks / (ms * 1e-3) / 1e9:.1f} Gbit/s raw in; "
+          f"{_lib.launch_info(q, n, nblocks)}")
 
 
 if __name__ == "__main__":
