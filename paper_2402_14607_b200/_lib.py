@@ -13,9 +13,11 @@ import threading
 from .errors import CapacityError, DeviceError, ExtensionMissingError
 
 _LIB_DIR = pathlib.Path(__file__).resolve().parent / "_lib"
-#: BX_LIB=checked loads the bounds-checked build (see csrc/bx_core.cuh, BX_CHECK)
-LIB_PATH = _LIB_DIR / ("libbx_b200_checked.so" if os.environ.get("BX_LIB") == "checked"
-                       else "libbx_b200.so")
+#: BX_LIB=checked loads the bounds-checked build (see csrc/bx_core.cuh, BX_CHECK);
+#: BX_LIB=/abs/path.so an experimental build (tools/build_variant.py)
+_BX_LIB = os.environ.get("BX_LIB", "")
+LIB_PATH = (pathlib.Path(_BX_LIB) if _BX_LIB.endswith(".so")
+            else _LIB_DIR / ("libbx_b200_checked.so" if _BX_LIB == "checked" else "libbx_b200.so"))
 
 BX_OK, BX_EINVAL, BX_ECUDA, BX_ERANGE = 0, -1, -2, -3
 
