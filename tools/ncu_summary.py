@@ -20,6 +20,8 @@ METRICS = [
     ("fma_pipe_pct", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
     ("lsu_pipe_pct", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
     ("warps_active_pct", "sm__warps_active.avg.pct_of_peak_sustained_active"),
+    ("l1tex_pct", "l1tex__throughput.avg.pct_of_peak_sustained_active"),
+    ("issue_pct", "sm__inst_issued.avg.pct_of_peak_sustained_active"),
     ("registers", "launch__registers_per_thread"),
     ("grid", "launch__grid_size"),
     ("block", "launch__block_size"),
@@ -63,14 +65,15 @@ def main():
         res[label] = summarise(path)
     with open(a.out + ".json", "w") as f:
         json.dump(res, f, indent=1)
-    lines = ["| workload | kernel | us | DRAM R+W MB | DRAM % | ALU % | FMA % | LSU % | warps % | regs |",
-             "|---|---|---|---|---|---|---|---|---|---|"]
+    lines = ["| workload | kernel | us | DRAM R+W MB | DRAM % | ALU % | FMA % | LSU % | L1 % | issue % | warps % | regs |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for label, ks in res.items():
         for k in ks:
             mb = (k.get("dram_read_bytes", 0) + k.get("dram_write_bytes", 0)) / 1e6
             lines.append(f"| {label} | {str(k.get('kernel'))[:40]} | {k.get('duration_us', 0):.1f} | {mb:.1f} | "
                          f"{k.get('dram_pct_peak', 0):.1f} | {k.get('alu_pipe_pct', 0):.1f} | "
                          f"{k.get('fma_pipe_pct', 0):.1f} | {k.get('lsu_pipe_pct', 0):.1f} | "
+                         f"{k.get('l1tex_pct', 0):.1f} | {k.get('issue_pct', 0):.1f} | "
                          f"{k.get('warps_active_pct', 0):.1f} | {k.get('registers', 0):.0f} |")
     with open(a.out + ".md", "w") as f:
         f.write("\n".join(lines) + "\n")
