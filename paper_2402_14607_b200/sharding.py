@@ -48,7 +48,8 @@ def _slice(buf, lo: int, hi: int):
     return buf[lo:hi]
 
 
-PIPE_CHUNK_BYTES = 64 << 20     # host->device pipeline granularity per stream
+# host->device pipeline granularity per stream (BX_PIPE_MB overrides)
+PIPE_CHUNK_BYTES = int(os.environ.get("BX_PIPE_MB", "64")) << 20
 
 
 def _as_tensor(buf):
