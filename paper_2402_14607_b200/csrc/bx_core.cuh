@@ -878,19 +878,7 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const 
       } else {
         Holes<Q> acc;
         acc.init();
-        if constexpr (Q == 128 && Holes<Q>::kPair) {
-          // one element per unit: pair consecutive units (elements)
-          int u = 0;
-#pragma unroll 1
-          for (; u + 1 < units; u += 2) {
-            const uint4 X0 = __ldg(xp + u), Y0 = __ldg(yp + u);
-            const uint4 X1 = __ldg(xp + u + 1), Y1 = __ldg(yp + u + 1);
-            const uint32_t a[4] = {X0.x, X0.y, X0.z, X0.w}, b[4] = {Y0.x, Y0.y, Y0.z, Y0.w};
-            const uint32_t c2[4] = {X1.x, X1.y, X1.z, X1.w}, d2[4] = {Y1.x, Y1.y, Y1.z, Y1.w};
-            acc.add2(a, b, c2, d2);
-          }
-          if (u < units) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
-        } else if constexpr (Q > 32) {
+        if constexpr (Q > 32) {
 #pragma unroll 1
           for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
         } else {
