@@ -18,6 +18,9 @@ device memory on long or unbounded inputs.
 """
 from __future__ import annotations
 
+import io
+import os
+import stat
 import time
 from dataclasses import dataclass
 from typing import Iterable, Iterator, Sequence
@@ -261,6 +264,19 @@ class _Source:
     def avail(self) -> int:
         return self.buffered * 8 - self.consumed
 
+    def known_bytes(self) -> int | None:
+        """Bytes this stream can still deliver, when knowable without reading
+        (in-memory inputs; regular files); None for pipes and sockets."""
+        if self._mem is not None:
+            return self._total - self.buffered
+        try:
+            st = os.fstat(self._file.fileno())
+            if not stat.S_ISREG(st.st_mode):
+                return None
+            return max(0, st.st_size - self._file.tell())
+        except (AttributeError, OSError, ValueError, io.UnsupportedOperation):
+            return None
+
     def _read(self, need: int) -> int:
         if self._mem is not None:
             got = min(need, self._total - self.buffered)
@@ -345,6 +361,8 @@ class Extraction:
         self._devices = list(devices) if devices else None
         self._segment = max(64, (int(segment_blocks) // 64) * 64)
         self._lazy = False               # __iter__: grow segments from FIRST_LAZY_SEGMENT
+        self._out_buf = None             # run(sink): whole-run pinned output (eq mode)
+        self._out_pos = 0
         self._started = False
         self._used_bits = 0
         self._stop_reason = "completed"
@@ -413,9 +431,16 @@ class Extraction:
 
         B = width * n
         lo, hi = bit // 8, (bit + count * B + 7) // 8
+        out = None
+        if self._out_buf is not None:
+            # run(sink), eq mode: D2H straight into the run's single output
+            # buffer (segments are multiples of 64 blocks, so every segment but
+            # the last ends on a byte boundary)
+            out = self._out_buf[self._out_pos:]
+            self._out_pos += (count * width) // 8
         return sharding.extract_packed(self._x.window(lo, hi), self._y.window(lo, hi), width, n,
                                        count, x_bit0=bit % 8, y_bit0=bit % 8,
-                                       device=self._device, devices=self._devices)
+                                       device=self._device, devices=self._devices, out=out)
 
     def _segments_eq(self) -> Iterator[tuple[int, int, bytes]]:
         """Yield (first_block, count, packed_output) segment by segment
@@ -507,6 +532,32 @@ class Extraction:
         if self._workers < 1:
             raise ValueError("workers must be >= 1")
 
+    #: largest single output buffer run(sink) preallocates (pinned host memory)
+    OUT_BUF_MAX = 4 << 30
+
+    def _alloc_out_buf(self) -> None:
+        """eq mode, more than one segment: one pinned buffer for the whole
+        output, so segments D2H into place and the sink gets one zero-copy
+        write (instead of joining per-segment buffers)."""
+        if self.mode != "eq" or self.plan.field_bits > MAX_FIELD_BITS:
+            return
+        width, B = self.plan.field_bits, self.plan.field_bits * self.plan.vec_len
+        blocks = self._block_limit()
+        for src in (self._x, self._y):
+            kb = src.known_bytes()
+            if kb is not None:
+                blocks = min(blocks, (8 * kb + src.avail()) // B)
+        if blocks <= self._segment:
+            return                      # one segment: its own buffer is already whole
+        nbytes = (blocks * width + 7) // 8
+        if nbytes > self.OUT_BUF_MAX:
+            return
+        import torch
+
+        self._out_buf = torch.empty(nbytes + 1, dtype=torch.uint8,
+                                    pin_memory=torch.cuda.is_available())
+        self._out_pos = 0
+
     def _seg_cap(self, done: int) -> int:
         """Blocks in the next segment.  ``run`` uses full segments; iteration
         starts at FIRST_LAZY_SEGMENT blocks and doubles, so the first chunks of
@@ -553,6 +604,8 @@ class Extraction:
         parts: list[bytes] = []
         carry = 0          # neq: bit-level concatenation of variable-width segments
         carry_bits = 0
+        if sink is not None:
+            self._alloc_out_buf()
         try:
             for first, count, packed in self._segments():
                 if self.mode == "eq":
@@ -561,7 +614,7 @@ class Extraction:
                     nbits = sum(self._widths[first:first + count])
                 self._chunks_emitted += count
                 self._output_bits += nbits
-                if sink is None:
+                if sink is None or self._out_buf is not None:
                     continue
                 if carry_bits == 0 and nbits % 8 == 0:
                     parts.append(packed)
@@ -575,7 +628,12 @@ class Extraction:
                         carry_bits -= 8 * whole
         finally:
             self._finalize()
-        if sink is not None:
+        if sink is not None and self._out_buf is not None:
+            nbytes = (self._output_bits + 7) // 8
+            sink.write(memoryview(self._out_buf.numpy()[:nbytes]))
+            self._out_buf = None
+            self.report.pad_bits = (-self._output_bits) % 8
+        elif sink is not None:
             if carry_bits:
                 parts.append(carry.to_bytes(1, "little"))
             if len(parts) == 1:

@@ -213,19 +213,25 @@ def extract_neq_packed(xv, yv, q1: int, step: int, n: int, count: int, *, device
 
 
 def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit0: int = 0,
-                   device=None, devices=None) -> np.ndarray:
+                   device=None, devices=None, out=None) -> np.ndarray:
     """Packed output of `count` blocks (uint8 array over pinned memory; the last
     byte is zero-padded); xv/yv hold the windows (host buffers or
     torch tensors) starting at bit x_bit0 / y_bit0 of their first byte.  With
     several devices the blocks are split into contiguous 64-aligned ranges, one
-    per device, each driven by its own host thread."""
+    per device, each driven by its own host thread.  `out` (a CPU uint8 tensor
+    of at least ceil(count*q/8) bytes, ideally pinned) receives the bytes
+    instead of a fresh pinned buffer."""
     from . import device as D
 
     import torch
 
     devs = [D.require_cuda(d) for d in devices] if devices else [D.require_cuda(device)]
     B = q * n
-    out = torch.empty((count * q + 7) // 8, dtype=torch.uint8, pin_memory=True)
+    obytes = (count * q + 7) // 8
+    if out is None:
+        out = torch.empty(obytes, dtype=torch.uint8, pin_memory=True)
+    else:
+        out = out[:obytes]
     ranges = [r for r in shard_ranges(count, len(devs)) if r[1] > 0]
     errors: list[BaseException] = []
 

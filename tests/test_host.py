@@ -16,16 +16,16 @@ import paper_2402_14607_b200 as bx
 from paper_2402_14607_b200 import _lib, sharding
 from oracle import coracle
 
-from bxtest_util import DribbleIO, case_inputs, report_dict, tiny_eq_plan
+from bxtest_util import DribbleIO, case_inputs, place, report_dict, tiny_eq_plan
 from conftest import REPO
 
 
 @pytest.fixture
 def oracle_compute(monkeypatch):
-    def fake(xv, yv, q, n, count, *, x_bit0=0, y_bit0=0, device=None, devices=None):
+    def fake(xv, yv, q, n, count, *, x_bit0=0, y_bit0=0, device=None, devices=None, out=None):
         xb = bytes(memoryview(xv).cast("B")) if not hasattr(xv, "numpy") else xv.numpy().tobytes()
         yb = bytes(memoryview(yv).cast("B")) if not hasattr(yv, "numpy") else yv.numpy().tobytes()
-        return coracle.extract_eq(xb, yb, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0)
+        return place(coracle.extract_eq(xb, yb, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0), out)
     monkeypatch.setattr(sharding, "extract_packed", fake)
 
     def fake_neq(xv, yv, q1, step, n, count, *, device=None):
@@ -165,6 +165,42 @@ def test_iteration_chunks_and_segments(golden, oracle_compute):
     assert run.cursor.block_index == len(chunks) + 1
     with pytest.raises(RuntimeError):
         list(run)
+
+
+@pytest.mark.parametrize("kind", ["bytes", "file", "dribble"])
+def test_multi_segment_run_single_buffer(golden, oracle_compute, tmp_path, kind):
+    """run(sink) over several segments: whole-run output buffer (in-memory and
+    regular-file sources, size known) or per-segment parts (pipe-like source):
+    the same bytes, one sink write, same report."""
+    c = next(c for c in golden("eq_cases.json") if c["tag"] == "multi_fill")
+    xb, yb = case_inputs(c)
+    plan = tiny_eq_plan(bx, c["b"], c["samples"], "3/4", c["n"], c["q"])
+    want = bx.extract_eq(xb, yb, plan).run(io.BytesIO())
+    if kind == "bytes":
+        src = (xb, yb)
+    elif kind == "file":
+        (tmp_path / "x").write_bytes(xb)
+        (tmp_path / "y").write_bytes(yb)
+        src = (open(tmp_path / "x", "rb"), open(tmp_path / "y", "rb"))
+    else:
+        src = (DribbleIO(xb, 1000), DribbleIO(yb, 777))
+
+    class OneWrite(io.BytesIO):
+        writes = 0
+
+        def write(self, b):
+            OneWrite.writes += 1
+            return super().write(b)
+
+    sink = OneWrite()
+    run = bx.extract_eq(*src, plan, segment_blocks=640)
+    rep = run.run(sink)
+    if kind == "file":
+        for f in src:
+            f.close()
+    assert sink.getvalue().hex() == c["out"]
+    assert OneWrite.writes == 1
+    assert report_dict(rep) == report_dict(want)
 
 
 def test_type_checks():

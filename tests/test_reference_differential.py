@@ -25,13 +25,14 @@ import paper_2402_14607_b200 as bx  # noqa: E402
 from paper_2402_14607_b200 import sharding  # noqa: E402
 from oracle import coracle  # noqa: E402
 
-from bxtest_util import DribbleIO, report_dict  # noqa: E402
+from bxtest_util import DribbleIO, place, report_dict  # noqa: E402
 
 
 @pytest.fixture(autouse=True)
 def oracle_compute(monkeypatch):
-    def fake(xv, yv, q, n, count, *, x_bit0=0, y_bit0=0, device=None, devices=None):
-        return coracle.extract_eq(bytes(xv), bytes(yv), q, n, count, x_bit0=x_bit0, y_bit0=y_bit0)
+    def fake(xv, yv, q, n, count, *, x_bit0=0, y_bit0=0, device=None, devices=None, out=None):
+        return place(coracle.extract_eq(bytes(xv), bytes(yv), q, n, count, x_bit0=x_bit0,
+                                        y_bit0=y_bit0), out)
 
     def fake_neq(xv, yv, q1, step, n, count, *, device=None):
         xb, yb = bytes(xv), bytes(yv)
