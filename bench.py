@@ -344,10 +344,15 @@ def run_ours(args, wl) -> None:
         bx.extract_eq(xs_, ys_, plan, device=dev).run(KeepSink())   # warm-up
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
+        marks = []
         for _ in range(e2e_steps):
             snk = KeepSink()
             rep = bx.extract_eq(xs_, ys_, plan, device=dev).run(snk)
+            marks.append(time.perf_counter())
         torch.cuda.synchronize(dev)
+        if os.environ.get("BX_BENCH_DEBUG"):
+            print("e2e step ms:", [round(1e3 * (b - a), 2) for a, b in zip([t0] + marks, marks)],
+                  file=sys.stderr)
         ok = snk.getvalue() == host_out and rep.blocks_completed == nblocks
         return (time.perf_counter() - t0) / e2e_steps, ok
 

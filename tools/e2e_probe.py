@@ -19,7 +19,7 @@ from paper_2402_14607_b200 import workloads as W
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c3")
-ap.add_argument("--sink", default="bytesio", choices=["bytesio", "null"])
+ap.add_argument("--sink", default="bytesio", choices=["bytesio", "null", "keep"])
 a = ap.parse_args()
 wl = W.WORKLOADS[a.workload]
 nb = wl.stream_bytes
@@ -33,7 +33,13 @@ class Null:
         return len(b)
 
 
-mk = io.BytesIO if a.sink == "bytesio" else Null
+class Keep:
+    def write(self, b):
+        self.data = b
+        return len(b)
+
+
+mk = {"bytesio": io.BytesIO, "null": Null, "keep": Keep}[a.sink]
 bx.extract_eq(x, y, plan).run(mk())
 torch.cuda.synchronize()
 for _ in range(2):
