@@ -130,10 +130,13 @@ class _Stager:
 
 
 def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0: int, dev,
-                        out: np.ndarray, out_byte0: int) -> None:
+                        out, out_byte0: int, dev_out=None) -> None:
     """`count` blocks on one device.  Host inputs are streamed in ~64 MiB chunks
     on a copy stream while earlier chunks compute (one launch per chunk); device
-    inputs are used in place (copied once if they lack the guard padding)."""
+    inputs are used in place (copied once if they lack the guard padding).
+    The packed output goes to host `out` at byte out_byte0 (D2H), or, with
+    ``dev_out = (tensor, bit0)``, straight from the kernels into that device
+    buffer (which may live on a peer GPU: NVLink stores, no D2H)."""
     import torch
 
     from . import device as D
@@ -144,11 +147,15 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
     obytes = (count * q + 7) // 8
     with torch.cuda.device(dev):
         comp = torch.cuda.current_stream(dev)
-        res = torch.zeros(D.padded_len(obytes), dtype=torch.uint8, device=dev)
+        if dev_out is None:
+            res, rbit = torch.zeros(D.padded_len(obytes), dtype=torch.uint8, device=dev), 0
+        else:
+            res, rbit = dev_out
         if xt.is_cuda and yt.is_cuda:
             xd = _device_view(xt, xn, dev)
             yd = _device_view(yt, yn, dev)
-            D.extract_eq(xd, xn, yd, yn, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0, out=res)
+            D.extract_eq(xd, xn, yd, yn, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0, out=res,
+                         out_bit0=rbit)
         else:
             xd = D.empty_stream(xn, dev)
             yd = D.empty_stream(yn, dev)
@@ -181,15 +188,16 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
                     comp.wait_stream(cx)
                     comp.wait_stream(cy)
                     D.extract_eq(xd, xn, yd, yn, q, n, cnt, x_bit0=xs, y_bit0=ys, out=res,
-                                 out_bit0=done * q, stream=comp)
+                                 out_bit0=rbit + done * q, stream=comp)
                     done += cnt
             finally:
                 if stager is not None:
                     stager.close()
             xd.record_stream(cx)
             yd.record_stream(cy)
-        # D2H straight into this range of the (pinned) result
-        out[out_byte0:out_byte0 + obytes].copy_(res[:obytes], non_blocking=True)
+        if dev_out is None:
+            # D2H straight into this range of the (pinned) result
+            out[out_byte0:out_byte0 + obytes].copy_(res[:obytes], non_blocking=True)
         comp.synchronize()
 
 
@@ -259,18 +267,33 @@ def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit
 
 
 def distributed_extract(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0,
-                        y_bit0: int = 0, group=None, compute=None, device=None) -> bytes | None:
+                        y_bit0: int = 0, group=None, compute=None, device=None,
+                        gather: str = "object", to_host: bool = True):
     """Multi-process form (one process per GPU, torch.distributed).
 
     Every rank sees the same run (e.g. a shared capture file or a shared seeded
-    generator) and computes only its contiguous block range ``rank_range``; the
-    packed parts are gathered to rank 0, which returns the concatenated output
-    (other ranks return None).  There is no collective on the data path: the
-    gather moves only the outputs (1/(2n) of the input bytes).
+    generator) and computes only its contiguous block range ``rank_range``;
+    rank 0 returns the whole packed output (other ranks return None).  There is
+    no collective on the input path; only outputs (1/(2n) of the input bytes)
+    move, in one of two ways:
 
-    ``compute`` defaults to :func:`extract_packed` on ``device``; tests inject a
-    stand-in to exercise the range/offset logic on CPU (gloo).
+    * ``gather="object"``: each rank's packed part (host bytes) is gathered to
+      rank 0 through the process group (any backend; ``compute`` lets CPU
+      tests inject a stand-in for the GPU step);
+    * ``gather="peer"``: rank 0 allocates the output in its HBM and shares it
+      over CUDA IPC; every rank's extraction kernels store their range of it
+      directly -- peer stores over NVLink from the kernel epilogue, so the
+      gather is fused into the compute and no extra collective or copy runs.
+      Ranges start at multiples of 64 blocks (64*q bits = whole 32-bit words),
+      so ranks never share an output word.  Rank 0 returns host bytes, or the
+      device tensor with ``to_host=False``.  Requires every process to see
+      rank 0's GPU under the same index (torchrun's default visibility).
     """
+    if gather == "peer":
+        return _distributed_extract_peer(xv, yv, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0,
+                                         group=group, device=device, to_host=to_host)
+    if gather != "object":
+        raise ValueError(f"unknown gather mode {gather!r}")
     import torch.distributed as dist
 
     rank = dist.get_rank(group)
@@ -293,3 +316,45 @@ def distributed_extract(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0,
             ob = s * q // 8
             out[ob:ob + len(p)] = p
     return bytes(out)
+
+
+def _distributed_extract_peer(xv, yv, q: int, n: int, count: int, *, x_bit0: int, y_bit0: int,
+                              group, device, to_host: bool):
+    """gather="peer" of :func:`distributed_extract`."""
+    import torch
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    from . import device as D
+
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    dev = D.require_cuda(device)
+    obytes = (count * q + 7) // 8
+    if rank == 0:
+        buf = torch.zeros(D.padded_len(obytes), dtype=torch.uint8, device=dev)
+        torch.cuda.synchronize(dev)       # zeroed before any peer stores into it
+        shared = [reduce_tensor(buf)]
+    else:
+        shared = [None]
+    dist.broadcast_object_list(shared, src=0, group=group)
+    if rank != 0:
+        rebuild, args = shared[0]
+        buf = rebuild(*args)              # rank 0's buffer mapped into this process
+    start, cnt = rank_range(count, rank, world)
+    B = q * n
+    if cnt:
+        xs, ys = x_bit0 + start * B, y_bit0 + start * B
+        _extract_one_device(_slice(xv, xs // 8, (xs + cnt * B + 7) // 8),
+                            _slice(yv, ys // 8, (ys + cnt * B + 7) // 8),
+                            q, n, cnt, xs % 8, ys % 8, dev, None, 0,
+                            dev_out=(buf, start * q))
+    torch.cuda.synchronize(dev)
+    dist.barrier(group=group)           # every range is in rank 0's buffer
+    if rank != 0:
+        del buf
+        dist.barrier(group=group)       # rank 0 may free the buffer after this
+        return None
+    dist.barrier(group=group)
+    res = buf[:obytes]
+    return res.cpu().numpy().tobytes() if to_host else res
