@@ -399,6 +399,10 @@ __device__ __forceinline__ void kara_fin(const uint32_t (&P)[K], Wide<CW>& c) {
   }
 }
 
+#ifndef BX_KPAIR_MAX_HALVES
+#define BX_KPAIR_MAX_HALVES 6   // pair two elements per accumulate step up to this many halves
+#endif
+
 template <int Q>
 struct Holes {
   static constexpr int EW = cdiv(Q, 32);       // 32-bit words per element
@@ -406,10 +410,10 @@ struct Holes {
   static constexpr int K = kara_leaves(NH);    // leaf half products per element
   static constexpr int CW = cdiv(2 * Q - 1, 32);
   // pairing two elements per accumulate step saves a LOP3 per residue but
-  // doubles the live operand parts; beyond 4 halves it would spill at the
-  // 128-register cap (an uncapped 255-register variant for q=128 measured 13%
-  // slower: 1250 vs 1432 GB/s at 8 warps/SM).
-  static constexpr bool kPair = NH <= 4;
+  // doubles the live operand parts: +3-6% up to 6 halves (q <= 96; measured
+  // profiles/r01_direct_sweep.txt H), none at 7-8 halves, where the register
+  // cap is the limit (an uncapped 255-register q=128 variant was 13% slower).
+  static constexpr bool kPair = NH <= BX_KPAIR_MAX_HALVES;
   uint32_t acc[K][3];
 
   __device__ __forceinline__ void init() {

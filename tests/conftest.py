@@ -26,3 +26,24 @@ def load_golden(name):
 @pytest.fixture(scope="session")
 def golden():
     return load_golden
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Under BX_LIB=checked (the bounds-checked library build), fail the session
+    if any kernel run in this process recorded an out-of-bounds index."""
+    import os
+    if os.environ.get("BX_LIB") != "checked":
+        return
+    from paper_2402_14607_b200 import _lib
+    if _lib._handle is None:
+        return
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return
+    except ImportError:
+        return
+    n, first = _lib.checked_violations()
+    print(f"\nchecked build: {n} bounds violations (first {first})")
+    if n:
+        session.exitstatus = 1

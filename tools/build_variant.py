@@ -32,6 +32,8 @@ def main():
         objs = list(ex.map(comp, srcs))
     lib = out / "libbx_b200.so"
     subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", str(lib), *map(str, objs)], check=True)
+    for o in objs:            # keep only the library (the snapshot travels to the GPU box)
+        o.unlink()
     print(lib)
 
 
