@@ -52,7 +52,11 @@ int bx_modulus_exponents(int q, int* exps);
  * to bits [out_bit0 + l*q, out_bit0 + (l+1)*q) of out.  Other bits of out are
  * preserved (boundary words are updated atomically).
  *
- * x, y, out: device pointers, 4-byte aligned.  x_bytes / y_bytes: bytes of
+ * x, y, out: device pointers, 4-byte aligned; the kernels run on the device
+ * that owns x, and out may be memory of a peer GPU mapped into this process
+ * (CUDA IPC / peer access: the outputs are then stored over NVLink -- how
+ * sharding.distributed_extract(gather="peer") gathers ranks' ranges into rank
+ * 0's buffer).  x_bytes / y_bytes: bytes of
  * valid stream data; the buffers must stay readable up to round_up(x_bytes, 16)
  * + 16 bytes (the TMA-bulk path copies whole 16-byte granules).  16-byte
  * aligned x and y select the aligned kernels (direct, or persistent TMA-bulk).
