@@ -854,10 +854,20 @@ __device__ __forceinline__ Wide<cdiv(2 * Q - 1, 32)> direct_block_wide(const uin
   return c;
 }
 
+#ifndef BX_PDL
+#define BX_PDL 1   // programmatic dependent launch for the direct kernel (0: plain launches, A/B)
+#endif
+
 template <int Q, int U>
 __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
+#if BX_PDL
+  // let the next launch in the stream get scheduled as this grid drains, and
+  // wait for the previous grid (complete, memory visible) before any access
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   Wide<EW> z = wzero<EW>();

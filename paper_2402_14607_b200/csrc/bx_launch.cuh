@@ -216,6 +216,25 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
       d.y_limit = a.y_limit / 4 - a.y_bit0 / 128;
       d.out_words = a.out_words - a.out_bit0 / 32;
       const dim3 g((unsigned)c.grid), b(c.threads);
+#if BX_PDL
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = g;
+      cfg.blockDim = b;
+      cfg.dynamicSmemBytes = 0;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      switch (c.units) {
+        case 1: return cudaLaunchKernelEx(&cfg, eq_direct_kernel<Q, 1>, d);
+        case 2: return cudaLaunchKernelEx(&cfg, eq_direct_kernel<Q, 2>, d);
+        case 4: return cudaLaunchKernelEx(&cfg, eq_direct_kernel<Q, 4>, d);
+        case 8: return cudaLaunchKernelEx(&cfg, eq_direct_kernel<Q, 8>, d);
+        default: return cudaLaunchKernelEx(&cfg, eq_direct_kernel<Q, 0>, d);
+      }
+#else
       switch (c.units) {
         case 1: eq_direct_kernel<Q, 1><<<g, b, 0, s>>>(d); break;
         case 2: eq_direct_kernel<Q, 2><<<g, b, 0, s>>>(d); break;
@@ -224,6 +243,7 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
         default: eq_direct_kernel<Q, 0><<<g, b, 0, s>>>(d); break;
       }
       return cudaGetLastError();
+#endif
     }
   }
   if (c.staged) {
