@@ -680,8 +680,23 @@ __device__ __forceinline__ TileWin tile_window(int64_t bit_start, int64_t nbits)
   return w;
 }
 
+#ifndef BX_PDL
+#define BX_PDL 1   // programmatic dependent launch for the direct and TMA kernels (0: plain, A/B)
+#endif
+
+// Programmatic dependent launch: allow the next launch in the stream to be
+// scheduled as this grid drains; wait for the previous grid (complete, memory
+// visible) before touching global memory.
+__device__ __forceinline__ void pdl_entry() {
+#if BX_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 template <int Q>
 __global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? 3 : 2))) eq_tma_kernel(const EqArgs a) {
+  pdl_entry();
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ __align__(8) uint64_t bars[2];
   const int T = a.tile_blocks;
@@ -854,20 +869,11 @@ __device__ __forceinline__ Wide<cdiv(2 * Q - 1, 32)> direct_block_wide(const uin
   return c;
 }
 
-#ifndef BX_PDL
-#define BX_PDL 1   // programmatic dependent launch for the direct kernel (0: plain launches, A/B)
-#endif
-
 template <int Q, int U>
 __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
-#if BX_PDL
-  // let the next launch in the stream get scheduled as this grid drains, and
-  // wait for the previous grid (complete, memory visible) before any access
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
+  pdl_entry();
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   Wide<EW> z = wzero<EW>();

@@ -198,8 +198,22 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
     const int64_t ntiles = (a.nblocks + c.tile - 1) / c.tile;
     const int64_t resident = (int64_t)sm_count() * (occ > 0 ? occ : 1);
     const int64_t grid = ntiles < resident ? ntiles : resident;
+#if BX_PDL
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(c.threads);
+    cfg.dynamicSmemBytes = c.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, a);
+#else
     k<<<(unsigned)grid, c.threads, c.smem, s>>>(a);
     return cudaGetLastError();
+#endif
   }
   if constexpr (Q == 1 || Q == 2 || Q == 4 || Q == 8 || Q == 16 || Q == 32 || Q == 64 || Q == 128) {
     if (c.direct) {
