@@ -177,9 +177,11 @@ __device__ __forceinline__ Wide<cdiv(Q, 32)> reduce(const Wide<CW>& c) {
 // --------------------------------------------------------------- bit access
 
 // 32 bits of an LSB-first word stream starting at bit `off` (word off>>5 + 1
-// must be readable).
-__device__ __forceinline__ uint32_t read32(const uint32_t* src, int64_t off, int64_t lim) {
-  const int64_t w = off >> 5;
+// must be readable).  T: int64_t for global streams, uint32_t for shared-memory
+// tiles (32-bit index math).
+template <typename T>
+__device__ __forceinline__ uint32_t read32(const uint32_t* src, T off, int64_t lim) {
+  const T w = off >> 5;
   BX_CHECK(w + 1, lim, 1);
   return __funnelshift_r(src[w], src[w + 1], (uint32_t)(off & 31));
 }
@@ -470,11 +472,19 @@ struct EqArgs {
   int64_t out_words;   // words of out the run may touch (checked builds)
 };
 
-template <int Q, int EW>
-__device__ __forceinline__ void read_elem(const uint32_t* src, int64_t off, int64_t lim,
+// One q-bit element at bit `off`: the EW + 1 covering words are loaded once and
+// funnel-shifted (word (off>>5) + EW must be readable).
+template <int Q, int EW, typename T>
+__device__ __forceinline__ void read_elem(const uint32_t* src, T off, int64_t lim,
                                           uint32_t (&w)[EW]) {
+  const T w0 = off >> 5;
+  const uint32_t sh = (uint32_t)(off & 31);
+  BX_CHECK(w0 + EW, lim, 1);
+  uint32_t r[EW + 1];
 #pragma unroll
-  for (int i = 0; i < EW; i++) w[i] = read32(src, off + 32 * i, lim);
+  for (int i = 0; i <= EW; i++) r[i] = src[w0 + i];
+#pragma unroll
+  for (int i = 0; i < EW; i++) w[i] = __funnelshift_r(r[i], r[i + 1], sh);
   if constexpr (Q % 32) w[EW - 1] &= (1u << (Q % 32)) - 1u;
 }
 
@@ -483,7 +493,7 @@ __device__ __forceinline__ void read_elem(const uint32_t* src, int64_t off, int6
 // starts at bit xbase / ybase, and ORs its q-bit output into `so` at bit
 // obase + grp*Q (so must be zeroed).  xlim / ylim / olim are the word bounds of
 // sx / sy / so (checked builds).  Ends with the caller's __syncthreads.
-template <int Q>
+template <int Q, typename T = int64_t>
 __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx, const uint32_t* sy,
                                              int64_t xbase, int64_t ybase, uint32_t* so,
                                              int64_t obase, int nb, int64_t xlim, int64_t ylim,
@@ -496,14 +506,14 @@ __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx
   const int grp = tid >> a.tpb_log2, sub = tid & (tpb - 1);
   Wide<CW> c = wzero<CW>();
   if (grp < nb) {
-    const int64_t xo = xbase + grp * B, yo = ybase + grp * B;
+    const T xo = (T)xbase + (T)grp * (T)B, yo = (T)ybase + (T)grp * (T)B;
     if constexpr (Q <= kDiagMaxQ) {
       using D = Diag<Q>;
       D acc;
       acc.init();
       const int nch = cdiv(a.n, D::E);
       for (int ch = sub; ch < nch; ch += tpb) {
-        const int64_t off = (int64_t)ch * D::EB;
+        const T off = (T)ch * (T)D::EB;
         const int valid = min(D::E, a.n - ch * D::E) * Q;
         const uint32_t m = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
         acc.add(read32(sx, xo + off, xlim) & m, read32(sy, yo + off, ylim));
@@ -515,16 +525,16 @@ __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx
       int j = sub;
       for (; Holes<Q>::kPair && j + tpb < a.n; j += 2 * tpb) {
         uint32_t xw[EW], yw[EW], xw2[EW], yw2[EW];
-        read_elem<Q>(sx, xo + (int64_t)j * Q, xlim, xw);
-        read_elem<Q>(sy, yo + (int64_t)j * Q, ylim, yw);
-        read_elem<Q>(sx, xo + (int64_t)(j + tpb) * Q, xlim, xw2);
-        read_elem<Q>(sy, yo + (int64_t)(j + tpb) * Q, ylim, yw2);
+        read_elem<Q>(sx, xo + (T)j * (T)Q, xlim, xw);
+        read_elem<Q>(sy, yo + (T)j * (T)Q, ylim, yw);
+        read_elem<Q>(sx, xo + (T)(j + tpb) * (T)Q, xlim, xw2);
+        read_elem<Q>(sy, yo + (T)(j + tpb) * (T)Q, ylim, yw2);
         acc.add2(xw, yw, xw2, yw2);
       }
       for (; j < a.n; j += tpb) {
         uint32_t xw[EW], yw[EW];
-        read_elem<Q>(sx, xo + (int64_t)j * Q, xlim, xw);
-        read_elem<Q>(sy, yo + (int64_t)j * Q, ylim, yw);
+        read_elem<Q>(sx, xo + (T)j * (T)Q, xlim, xw);
+        read_elem<Q>(sy, yo + (T)j * (T)Q, ylim, yw);
         acc.add(xw, yw);
       }
       c = acc.unreduced();
@@ -617,7 +627,10 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_kernel(const EqArgs 
   __syncthreads();
   const int64_t xlim = STAGED ? a.stage_words : a.x_limit;
   const int64_t ylim = STAGED ? a.stage_words : a.y_limit;
-  tile_compute<Q>(a, sx, sy, xbase, ybase, so, ostart & 31, nb, xlim, ylim, ow + 1);
+  if constexpr (STAGED)
+    tile_compute<Q, uint32_t>(a, sx, sy, xbase, ybase, so, ostart & 31, nb, xlim, ylim, ow + 1);
+  else
+    tile_compute<Q, int64_t>(a, sx, sy, xbase, ybase, so, ostart & 31, nb, xlim, ylim, ow + 1);
   __syncthreads();
   tile_store(a.out, so, ostart, ostart + (int64_t)nb * Q, a.out_words);
 }
@@ -752,7 +765,7 @@ __global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? 3 : 2))) eq_tma_k
     mbar_wait(&bars[st], phase[st]);
     phase[st] ^= 1u;
     __syncthreads();
-    tile_compute<Q>(a, bufs + (2 * st) * sw, bufs + (2 * st + 1) * sw, wx.bit0, wy.bit0, so,
+    tile_compute<Q, uint32_t>(a, bufs + (2 * st) * sw, bufs + (2 * st + 1) * sw, wx.bit0, wy.bit0, so,
                     ostart & 31, nb, sw, sw, ow_max);
     __syncthreads();
     tile_store(a.out, so, ostart, ostart + (int64_t)nb * Q, a.out_words);

@@ -151,6 +151,7 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
             res, rbit = torch.zeros(D.padded_len(obytes), dtype=torch.uint8, device=dev), 0
         else:
             res, rbit = dev_out
+        co = None
         if xt.is_cuda and yt.is_cuda:
             xd = _device_view(xt, xn, dev)
             yd = _device_view(yt, yn, dev)
@@ -166,6 +167,11 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
             # threads (see _Stager) so their H2D is asynchronous too
             cx = torch.cuda.Stream(dev)
             cy = torch.cuda.Stream(dev)
+            # each chunk's output words go back on their own stream as soon as
+            # the chunk's kernel finished (D2H overlaps the next chunks' H2D:
+            # PCIe is full duplex); chunk boundaries sit on multiples of 64
+            # blocks, i.e. on whole output words, so chunks never share a word
+            co = torch.cuda.Stream(dev) if dev_out is None and out.is_pinned() else None
             stager = None if pinned else _Stager(int(os.environ.get("BX_STAGE_MB", "32")) << 20)
             step = max(ALIGN_BLOCKS, (PIPE_CHUNK_BYTES * 8 // B) // ALIGN_BLOCKS * ALIGN_BLOCKS)
             if stager is not None:
@@ -189,13 +195,21 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
                     comp.wait_stream(cy)
                     D.extract_eq(xd, xn, yd, yn, q, n, cnt, x_bit0=xs, y_bit0=ys, out=res,
                                  out_bit0=rbit + done * q, stream=comp)
+                    if co is not None:
+                        olo, ohi = done * q // 8, ((done + cnt) * q + 7) // 8
+                        co.wait_stream(comp)
+                        with torch.cuda.stream(co):
+                            out[out_byte0 + olo:out_byte0 + ohi].copy_(res[olo:ohi], non_blocking=True)
                     done += cnt
             finally:
                 if stager is not None:
                     stager.close()
             xd.record_stream(cx)
             yd.record_stream(cy)
-        if dev_out is None:
+            if co is not None:
+                res.record_stream(co)
+                co.synchronize()
+        if dev_out is None and co is None:
             # D2H straight into this range of the (pinned) result
             out[out_byte0:out_byte0 + obytes].copy_(res[:obytes], non_blocking=True)
         comp.synchronize()

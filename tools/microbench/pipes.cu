@@ -100,6 +100,54 @@ __global__ void k_mix32(uint32_t* out, uint32_t s) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = r;
 }
 
+
+#define CHAIN_KERNEL(NAME, ASM, ...)                                            \
+  __global__ void NAME(uint32_t* out, uint32_t s) {                            \
+    uint32_t a[ILP], b = s * 2654435761u + threadIdx.x, c = s ^ 0x9e3779b9u;    \
+    for (int i = 0; i < ILP; i++) a[i] = threadIdx.x * (i + 1) + s;            \
+    for (int it = 0; it < ITERS; it++) {                                       \
+      _Pragma("unroll") for (int i = 0; i < ILP; i++) {                        \
+        asm volatile(ASM : "+r"(a[i]) : "r"(b), "r"(c));                       \
+      }                                                                        \
+    }                                                                          \
+    uint32_t r = 0;                                                            \
+    for (int i = 0; i < ILP; i++) r ^= a[i];                                   \
+    out[blockIdx.x * blockDim.x + threadIdx.x] = r;                            \
+  }
+
+// 2-register IMAD (a*b + RZ), IMAD with immediate multiplier, IMAD.HI,
+// LOP3 with an immediate operand, PRMT, IADD3, FFMA (3-reg and immediate),
+// HFMA2, POPC.  "%1, %2" are registers; the chains keep a[i] dependent.
+CHAIN_KERNEL(k_mul2, "mul.lo.u32 %0, %0, %1;")
+CHAIN_KERNEL(k_imadimm, "mad.lo.u32 %0, %0, 0x9249, %2;")
+CHAIN_KERNEL(k_mulhi, "mul.hi.u32 %0, %0, %1;")
+CHAIN_KERNEL(k_lop3imm, "lop3.b32 %0, %0, 0x92492492, %2, 0x78;")
+CHAIN_KERNEL(k_lop3imm2, "and.b32 %0, %0, 0x92492492;")
+CHAIN_KERNEL(k_prmt, "prmt.b32 %0, %0, %1, 0x5410;")
+CHAIN_KERNEL(k_iadd3, "add.u32 %0, %0, %1;")
+CHAIN_KERNEL(k_ffma, "fma.rn.f32 %0, %0, %1, %2;")
+CHAIN_KERNEL(k_ffmaimm, "fma.rn.f32 %0, %0, 0f3F800001, %2;")
+CHAIN_KERNEL(k_hfma2, "fma.rn.f16x2 %0, %0, %1, %2;")
+CHAIN_KERNEL(k_popc, "popc.b32 %0, %0;")
+CHAIN_KERNEL(k_shl_imad, "shl.b32 %0, %0, 3;")
+
+// mixes: one 2-reg IMAD + one 3-reg LOP3; two LOP3 + one IMAD
+__global__ void k_mix_mul2_lop(uint32_t* out, uint32_t s) {
+  uint32_t a[ILP], l[ILP];
+  uint32_t b = s * 2654435761u + threadIdx.x, c = s ^ 0x9e3779b9u;
+  for (int i = 0; i < ILP; i++) { a[i] = threadIdx.x * (i + 1) + s; l[i] = a[i] * 3u; }
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int i = 0; i < ILP; i++) {
+      asm volatile("mul.lo.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(b));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x78;" : "+r"(l[i]) : "r"(b), "r"(c));
+    }
+  }
+  uint32_t r = 0;
+  for (int i = 0; i < ILP; i++) r ^= a[i] ^ l[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+
 typedef void (*kfn)(uint32_t*, uint32_t);
 
 static void run(const char* name, kfn f, double ops_per_step, int sms, int clk_khz) {
@@ -128,5 +176,18 @@ int main() {
   run("imad.wide", k_imadwide, 1, p.multiProcessorCount, clk);
   run("mix_wide", k_mix, 2, p.multiProcessorCount, clk);
   run("mix32", k_mix32, 2, p.multiProcessorCount, clk);
+  run("mul2", k_mul2, 1, p.multiProcessorCount, clk);
+  run("imad_imm", k_imadimm, 1, p.multiProcessorCount, clk);
+  run("mul.hi", k_mulhi, 1, p.multiProcessorCount, clk);
+  run("lop3_imm", k_lop3imm, 1, p.multiProcessorCount, clk);
+  run("and_imm", k_lop3imm2, 1, p.multiProcessorCount, clk);
+  run("prmt", k_prmt, 1, p.multiProcessorCount, clk);
+  run("iadd", k_iadd3, 1, p.multiProcessorCount, clk);
+  run("ffma", k_ffma, 1, p.multiProcessorCount, clk);
+  run("ffma_imm", k_ffmaimm, 1, p.multiProcessorCount, clk);
+  run("hfma2", k_hfma2, 1, p.multiProcessorCount, clk);
+  run("popc", k_popc, 1, p.multiProcessorCount, clk);
+  run("shl_imm", k_shl_imad, 1, p.multiProcessorCount, clk);
+  run("mul2+lop3", k_mix_mul2_lop, 2, p.multiProcessorCount, clk);
   return 0;
 }
