@@ -792,6 +792,17 @@ struct DirectArgs {
   int64_t out_words;   // writable words from out (checked builds)
 };
 
+// Pairing two elements per accumulate step (Holes::add2): same LOP3 count
+// after ptxas re-associates the XOR trees, but a different schedule.  At
+// q = 16 the unpaired order is 5% faster; at q = 32 / 64 the paired one is
+// equal / 3-5% faster (profiles/r01_direct_sweep.txt D).
+#ifndef BX_DIRECT_PAIR
+#define BX_DIRECT_PAIR 1
+#endif
+#ifndef BX_DIRECT_PAIR16
+#define BX_DIRECT_PAIR16 0
+#endif
+
 template <int Q>
 __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void* accp) {
   if constexpr (Q <= kDiagMaxQ) {
@@ -810,9 +821,14 @@ __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void
       for (int i = 0; i < 4; i++) {
         const uint32_t a0[1] = {xs[i]}, b0[1] = {ys[i]};          // low half (split masks it)
         const uint32_t a1[1] = {xs[i] >> 16}, b1[1] = {ys[i] >> 16};
+#if BX_DIRECT_PAIR16
         acc.add2(a0, b0, a1, b1);
+#else
+        acc.add(a0, b0);
+        acc.add(a1, b1);
+#endif
       }
-    } else if constexpr (4 / EW >= 2 && Holes<Q>::kPair) {
+    } else if constexpr (4 / EW >= 2 && Holes<Q>::kPair && BX_DIRECT_PAIR) {
 #pragma unroll
       for (int e = 0; e < 4 / EW; e += 2) {
         uint32_t a[EW], b[EW], c2[EW], d2[EW];
@@ -826,13 +842,16 @@ __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void
         acc.add2(a, b, c2, d2);
       }
     } else {
-      uint32_t a[EW], b[EW];
 #pragma unroll
-      for (int i = 0; i < EW; i++) {
-        a[i] = xs[i];
-        b[i] = ys[i];
+      for (int e = 0; e < 4 / EW; e++) {          // every element of the unit
+        uint32_t a[EW], b[EW];
+#pragma unroll
+        for (int i = 0; i < EW; i++) {
+          a[i] = xs[e * EW + i];
+          b[i] = ys[e * EW + i];
+        }
+        acc.add(a, b);
       }
-      acc.add(a, b);
     }
   }
 }
@@ -882,8 +901,16 @@ __device__ __forceinline__ Wide<cdiv(2 * Q - 1, 32)> direct_block_wide(const uin
   return c;
 }
 
+// Min resident CTAs for the q = 17..32 direct kernels: 3 caps them at 85
+// registers (127 uncapped, 2 CTAs/SM) without spills: +9% at q = 32
+// (profiles/r01_direct_sweep.txt E).
+#ifndef BX_DIRECT_MINB_Q32
+#define BX_DIRECT_MINB_Q32 3
+#endif
+
 template <int Q, int U>
-__global__ void __launch_bounds__(256, (Q > 32 ? 2 : 1)) eq_direct_kernel(const DirectArgs a) {
+__global__ void __launch_bounds__(256, (Q > 32 ? 2 : (Q > 16 ? BX_DIRECT_MINB_Q32 : 1)))
+    eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
   pdl_entry();
