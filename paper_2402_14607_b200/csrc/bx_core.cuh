@@ -795,7 +795,7 @@ struct DirectArgs {
 // Pairing two elements per accumulate step (Holes::add2): same LOP3 count
 // after ptxas re-associates the XOR trees, but a different schedule.  At
 // q = 16 the unpaired order is 5% faster; at q = 32 / 64 the paired one is
-// equal / 3-5% faster (profiles/r01_direct_sweep.txt D).
+// equal / 3-5% faster (profiles/r01_direct_sweep.txt J).
 #ifndef BX_DIRECT_PAIR
 #define BX_DIRECT_PAIR 1
 #endif
@@ -903,7 +903,7 @@ __device__ __forceinline__ Wide<cdiv(2 * Q - 1, 32)> direct_block_wide(const uin
 
 // Min resident CTAs for the q = 17..32 direct kernels: 3 caps them at 85
 // registers (127 uncapped, 2 CTAs/SM) without spills: +9% at q = 32
-// (profiles/r01_direct_sweep.txt E).
+// (profiles/r01_direct_sweep.txt K).
 #ifndef BX_DIRECT_MINB_Q32
 #define BX_DIRECT_MINB_Q32 3
 #endif

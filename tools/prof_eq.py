@@ -25,16 +25,21 @@ def main():
     ap.add_argument("--n", type=int)
     ap.add_argument("--blocks", type=int)
     ap.add_argument("--launches", type=int, default=3)
+    ap.add_argument("--real", action="store_true", help="the workload's seeded streams instead of random bytes")
     a = ap.parse_args()
     wl = W.WORKLOADS[a.workload]
     q, n = a.q or wl.q, a.n or wl.n
     nblocks = a.blocks or wl.num_blocks
     nbytes = (nblocks * q * n + 7) // 8
     g = torch.Generator(device="cuda").manual_seed(0)
-    x = D.empty_stream(nbytes, "cuda")
-    y = D.empty_stream(nbytes, "cuda")
-    x[:nbytes] = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device="cuda", generator=g)
-    y[:nbytes] = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device="cuda", generator=g)
+    if a.real:
+        x, _ = W.stream_device(wl.x, wl.samples, torch.device("cuda"))
+        y, _ = W.stream_device(wl.y, wl.samples, torch.device("cuda"))
+    else:
+        x = D.empty_stream(nbytes, "cuda")
+        y = D.empty_stream(nbytes, "cuda")
+        x[:nbytes] = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device="cuda", generator=g)
+        y[:nbytes] = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device="cuda", generator=g)
     out = torch.zeros(D.padded_len((nblocks * q + 7) // 8), dtype=torch.uint8, device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     D.extract_eq(x, nbytes, y, nbytes, q, n, nblocks, out=out)
