@@ -904,12 +904,83 @@ __device__ __forceinline__ Wide<cdiv(2 * Q - 1, 32)> direct_block_wide(const uin
 // Min resident CTAs for the q = 17..32 direct kernels: 3 caps them at 85
 // registers (127 uncapped, 2 CTAs/SM) without spills: +9% at q = 32
 // (profiles/r01_direct_sweep.txt K).
+// q = 128 in three passes over the block (BX_Q128_PASSES=0: one pass).  The
+// top Karatsuba level (64-bit halves) is taken outside the element loop:
+//     x*y = L + (L + H + M) t^64 + H t^128,  L = lo*lo, H = hi*hi, M = (lo^hi)*(hi^lo),
+// each summed over the block's elements by its own pass, so only one 64-bit
+// sub-product's 27 accumulators are live (the one-pass form keeps 81, which
+// forbids element pairing under the 128-register cap).  The block's 2 x 256
+// bytes are re-read from L1/L2 by passes 2 and 3.
+#ifndef BX_Q128_PASSES
+#define BX_Q128_PASSES 1
+#endif
+
+template <int P>
+__device__ __forceinline__ void q128_part(const uint4& v, uint32_t (&o)[2]) {
+  if constexpr (P == 0) {
+    o[0] = v.x;
+    o[1] = v.y;
+  } else if constexpr (P == 1) {
+    o[0] = v.z;
+    o[1] = v.w;
+  } else {
+    o[0] = v.x ^ v.z;
+    o[1] = v.y ^ v.w;
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void q128_pass(const uint4* xp, const uint4* yp, int units, Wide<8>& c) {
+  Holes<64> acc;
+  acc.init();
+  int u = 0;
+#pragma unroll 1
+  for (; u + 1 < units; u += 2) {
+    const uint4 X0 = __ldg(xp + u), Y0 = __ldg(yp + u);
+    const uint4 X1 = __ldg(xp + u + 1), Y1 = __ldg(yp + u + 1);
+    uint32_t a[2], b[2], a2[2], b2[2];
+    q128_part<P>(X0, a);
+    q128_part<P>(Y0, b);
+    q128_part<P>(X1, a2);
+    q128_part<P>(Y1, b2);
+    acc.add2(a, b, a2, b2);
+  }
+  if (u < units) {
+    uint32_t a[2], b[2];
+    q128_part<P>(__ldg(xp + u), a);
+    q128_part<P>(__ldg(yp + u), b);
+    acc.add(a, b);
+  }
+  const Wide<4> p = acc.unreduced();
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    if constexpr (P == 0) c.w[i] ^= p.w[i];          // L at t^0
+    if constexpr (P == 1) c.w[i + 4] ^= p.w[i];      // H at t^128
+    c.w[i + 2] ^= p.w[i];                            // L, H, M at t^64
+  }
+}
+
+__device__ __forceinline__ Wide<8> direct_block_q128(const uint4* xp, const uint4* yp, int units) {
+  Wide<8> c = wzero<8>();
+  q128_pass<0>(xp, yp, units, c);
+  q128_pass<1>(xp, yp, units, c);
+  q128_pass<2>(xp, yp, units, c);
+  return c;
+}
+
 #ifndef BX_DIRECT_MINB_Q32
 #define BX_DIRECT_MINB_Q32 3
 #endif
 
+// q = 128 (three passes): 3 CTAs/SM (80 registers) for 8 or more units per
+// block (c3 n=8: +4% over one pass), 2 below (n=4: 3 CTAs cost 13%, 2 gain
+// 12%) -- profiles/r01_direct_sweep.txt L.
+#ifndef BX_DIRECT_MINB_Q128
+#define BX_DIRECT_MINB_Q128(U) ((U) == 0 || (U) >= 8 ? 3 : 2)
+#endif
+
 template <int Q, int U>
-__global__ void __launch_bounds__(256, (Q > 32 ? 2 : (Q > 16 ? BX_DIRECT_MINB_Q32 : 1)))
+__global__ void __launch_bounds__(256, (Q == 128 ? BX_DIRECT_MINB_Q128(U) : (Q > 32 ? 2 : (Q > 16 ? BX_DIRECT_MINB_Q32 : 1))))
     eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
@@ -936,16 +1007,20 @@ __global__ void __launch_bounds__(256, (Q > 32 ? 2 : (Q > 16 ? BX_DIRECT_MINB_Q3
         for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
         c.w[0] = acc.unreduced();
       } else {
-        Holes<Q> acc;
-        acc.init();
-        if constexpr (Q > 32) {
-#pragma unroll 1
-          for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+        if constexpr (Q == 128 && BX_Q128_PASSES) {
+          c = direct_block_q128(xp, yp, units);
         } else {
+          Holes<Q> acc;
+          acc.init();
+          if constexpr (Q > 32) {
+#pragma unroll 1
+            for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+          } else {
 #pragma unroll 2
-          for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+            for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+          }
+          c = acc.unreduced();
         }
-        c = acc.unreduced();
       }
       z = reduce<Q>(c);
     }
