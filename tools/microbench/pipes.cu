@@ -148,6 +148,34 @@ __global__ void k_mix_mul2_lop(uint32_t* out, uint32_t s) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = r;
 }
 
+
+// FP64 pipe: DFMA chain, and a 3-way mix DFMA + IMAD + LOP3 (is fp64 a third pipe?)
+__global__ void k_dfma(uint32_t* out, uint32_t s) {
+  double a[ILP], b = 1.0000001 + s * 1e-9, c = 1e-7;
+  for (int i = 0; i < ILP; i++) a[i] = threadIdx.x * (i + 1) + s;
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int i = 0; i < ILP; i++) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(a[i]) : "d"(b), "d"(c));
+  }
+  double r = 0; for (int i = 0; i < ILP; i++) r += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (uint32_t)r;
+}
+__global__ void k_mix3(uint32_t* out, uint32_t s) {
+  double d[ILP], b = 1.0000001 + s * 1e-9, c = 1e-7;
+  uint32_t m[ILP], l[ILP], bb = s * 2654435761u + threadIdx.x, cc = s ^ 0x9e3779b9u;
+  for (int i = 0; i < ILP; i++) { d[i] = threadIdx.x * (i + 1) + s; m[i] = threadIdx.x + i; l[i] = m[i] * 3u; }
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int i = 0; i < ILP; i++) {
+      asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(d[i]) : "d"(b), "d"(c));
+      asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(m[i]) : "r"(bb), "r"(cc));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x78;" : "+r"(l[i]) : "r"(bb), "r"(cc));
+    }
+  }
+  double r = 0; uint32_t q = 0; for (int i = 0; i < ILP; i++) { r += d[i]; q ^= m[i] ^ l[i]; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (uint32_t)r ^ q;
+}
+
 typedef void (*kfn)(uint32_t*, uint32_t);
 
 static void run(const char* name, kfn f, double ops_per_step, int sms, int clk_khz) {
@@ -189,5 +217,7 @@ int main() {
   run("popc", k_popc, 1, p.multiProcessorCount, clk);
   run("shl_imm", k_shl_imad, 1, p.multiProcessorCount, clk);
   run("mul2+lop3", k_mix_mul2_lop, 2, p.multiProcessorCount, clk);
+  run("dfma", k_dfma, 1, p.multiProcessorCount, clk);
+  run("dfma+imad+lop3", k_mix3, 3, p.multiProcessorCount, clk);
   return 0;
 }
