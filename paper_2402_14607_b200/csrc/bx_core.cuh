@@ -563,13 +563,17 @@ __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx
 
 // Store the assembled output words of one tile: interior words plainly, the
 // (<= 2) boundary words merged atomically so bits outside the run survive.
-__device__ __forceinline__ void tile_store(uint32_t* out, const uint32_t* so, int64_t ostart,
+// CLEAR: leave the tile's words of `so` zeroed for the buffer's next use (every
+// word a tile's blocks can touch lies in [0, ow)).
+template <bool CLEAR = false>
+__device__ __forceinline__ void tile_store(uint32_t* out, uint32_t* so, int64_t ostart,
                                            int64_t oend, int64_t out_words) {
   const int64_t gw0 = ostart >> 5;
   const int ow = (int)(((oend + 31) >> 5) - gw0);
   for (int i = threadIdx.x; i < ow; i += blockDim.x) {
     const int64_t lo = (gw0 + i) * 32, hi = lo + 32;
     const uint32_t v = so[i];
+    if constexpr (CLEAR) so[i] = 0u;
     BX_CHECK(gw0 + i, out_words, 3);
     if (lo >= ostart && hi <= oend) {
       out[gw0 + i] = v;
@@ -741,6 +745,10 @@ __global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? 3 : 2))) eq_tma_k
     mbar_init(&bars[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // both output tiles start zeroed; afterwards tile_store<true> re-zeroes the
+  // words it consumed, so a tile needs no zeroing pass (and no barrier) before
+  // its blocks OR their outputs in
+  for (int i = threadIdx.x; i < 2 * ow_max; i += blockDim.x) outs[i] = 0u;
   __syncthreads();
   int64_t t = blockIdx.x;
   if (threadIdx.x == 0 && t < ntiles) issue(t, 0);
@@ -759,16 +767,18 @@ __global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? 3 : 2))) eq_tma_k
     const int nb = (int)((a.nblocks - tile0) < T ? (a.nblocks - tile0) : T);
     const int64_t ostart = a.out_bit0 + tile0 * Q;
     uint32_t* so = outs + st * ow_max;
-    for (int i = threadIdx.x; i < ow_max; i += blockDim.x) so[i] = 0u;
     const TileWin wx = tile_window(a.x_bit0 + tile0 * B, (int64_t)nb * B);
     const TileWin wy = tile_window(a.y_bit0 + tile0 * B, (int64_t)nb * B);
+    // every thread observes the phase flip itself, which makes the bulk copy's
+    // bytes visible to it: no CTA barrier before the compute
     mbar_wait(&bars[st], phase[st]);
     phase[st] ^= 1u;
-    __syncthreads();
     tile_compute<Q, uint32_t>(a, bufs + (2 * st) * sw, bufs + (2 * st + 1) * sw, wx.bit0, wy.bit0, so,
                     ostart & 31, nb, sw, sw, ow_max);
+    // all of this tile's output bits are in `so` and all reads of this input
+    // buffer are done (thread 0 refills it next iteration)
     __syncthreads();
-    tile_store(a.out, so, ostart, ostart + (int64_t)nb * Q, a.out_words);
+    tile_store<true>(a.out, so, ostart, ostart + (int64_t)nb * Q, a.out_words);
   }
 }
 
