@@ -197,6 +197,31 @@ def test_device_tensor_inputs_and_segments():
             assert sink.getvalue() == want
 
 
+def test_host_pipeline_chunking(monkeypatch):
+    """Host inputs stream through the chunked H2D pipeline: pageable inputs via
+    the run-ahead pinned rings (many chunks, ring wrap-around), pinned inputs
+    via the two copy streams, each chunk's output D2H on its own stream; every
+    chunking gives the oracle's bytes, at byte-aligned and odd bit offsets."""
+    rnd = random.Random(22)
+    q, n = 56, 48
+    k = 3 * 64 * 40 + 17                     # ~2.7 MB per stream, a ragged last chunk
+    for lead in (0, 3):                      # odd start bits: x_bit0 = y_bit0 = lead
+        nb = (lead + k * q * n + 7) // 8
+        xb, yb = rnd.randbytes(nb), rnd.randbytes(nb)
+        want = coracle.extract_eq(xb, yb, q, n, k, x_bit0=lead, y_bit0=lead)
+        from paper_2402_14607_b200 import sharding
+        for mb in ("1", "128"):
+            monkeypatch.setenv("BX_STAGE_MB", mb)
+            got = sharding.extract_packed(xb, yb, q, n, k, x_bit0=lead, y_bit0=lead)
+            assert got.tobytes()[:len(want)] == want, ("pageable", mb, lead)
+        monkeypatch.setattr(sharding, "PIPE_CHUNK_BYTES", 1 << 20)
+        xt = torch.frombuffer(bytearray(xb), dtype=torch.uint8).pin_memory()
+        yt = torch.frombuffer(bytearray(yb), dtype=torch.uint8).pin_memory()
+        got = sharding.extract_packed(xt, yt, q, n, k, x_bit0=lead, y_bit0=lead)
+        assert got.tobytes()[:len(want)] == want, ("pinned", lead)
+        monkeypatch.setattr(sharding, "PIPE_CHUNK_BYTES", 64 << 20)
+
+
 def test_pack_kats(golden):
     for c in golden("pack.json"):
         vals = np.array([int(v, 16) for v in c["values"]], dtype=np.uint64)
