@@ -184,6 +184,8 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
 
     from . import device as D
 
+    if count <= 0:
+        return
     B = q * n
     xt, yt = _as_tensor(xv), _as_tensor(yv)
     xn, yn = (x_bit0 + count * B + 7) // 8, (y_bit0 + count * B + 7) // 8

@@ -42,3 +42,17 @@ for chunk in (n, 64 << 20, 16 << 20):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
     print(f"pinned x+y on two streams, {chunk >> 20} MiB chunks: {2 * n / dt / 1e9:.1f} GB/s")
+
+# the same 2 x 256 MiB over 4 streams (each operand split in halves)
+ss = [torch.cuda.Stream() for _ in range(4)]
+half = n // 2
+for rep in range(3):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for i, (d, h) in enumerate(((dx, hx), (dy, hy))):
+        for j in range(2):
+            with torch.cuda.stream(ss[2 * i + j]):
+                d[j * half:(j + 1) * half].copy_(h[j * half:(j + 1) * half], non_blocking=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+print(f"pinned x+y on four streams: {2 * n / dt / 1e9:.1f} GB/s")
