@@ -1065,4 +1065,111 @@ __global__ void __launch_bounds__(256, (Q == 128 ? BX_DIRECT_MINB_Q128(U) : (Q >
   }
 }
 
+
+// ------------------------------------------------------- period kernel
+//
+// Aligned fast path for q = 24, 40, 48, 56 (multiples of 8 that are not powers
+// of two; q*n a multiple of 128, 16-byte aligned windows, word-aligned output):
+// element starts repeat every lcm(q, 128) bits, a "period" of q/g 128-bit units
+// holding 128/g elements (g = gcd(q, 128); q = 56: 7 units, 16 elements).  One
+// thread per block loads a period's units straight from HBM and extracts every
+// element with compile-time funnel shifts -- no shared-memory staging, no
+// runtime bit offsets, no tile barriers (what the TMA kernel pays for arbitrary
+// offsets).  A warp's 32 consecutive outputs are 32*q bits = q whole words,
+// assembled in a per-warp shared buffer.
+__host__ __device__ constexpr int cgcd(int a, int b) { return b ? cgcd(b, a % b) : a; }
+
+__host__ __device__ constexpr bool period_q(int q) {
+  return q == 24 || q == 40 || q == 48 || q == 56;
+}
+
+#ifndef BX_PERIOD_MINB
+#define BX_PERIOD_MINB 2
+#endif
+
+template <int Q>
+__global__ void __launch_bounds__(256, BX_PERIOD_MINB) eq_period_kernel(const DirectArgs a) {
+  constexpr int EW = cdiv(Q, 32);
+  constexpr int G = cgcd(Q, 128);
+  constexpr int UNITS = Q / G;          // 128-bit units per period
+  constexpr int ELEMS = 128 / G;        // elements per period (even)
+  constexpr int WORDS = 4 * UNITS;
+  __shared__ uint32_t sout[8][Q + 1];
+  pdl_entry();
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Wide<EW> z = wzero<EW>();
+  if (l < a.nblocks) {
+    const uint4* xp = a.x + l * a.units;
+    const uint4* yp = a.y + l * a.units;
+    BX_CHECK((l + 1) * a.units - 1, a.x_limit, 7);
+    BX_CHECK((l + 1) * a.units - 1, a.y_limit, 7);
+    Holes<Q> acc;
+    acc.init();
+    const int periods = a.units / UNITS;
+#pragma unroll 1
+    for (int p = 0; p < periods; p++) {
+      uint32_t xw[WORDS], yw[WORDS];
+#pragma unroll
+      for (int u = 0; u < UNITS; u++) {
+        const uint4 X = __ldg(xp + p * UNITS + u), Y = __ldg(yp + p * UNITS + u);
+        xw[4 * u] = X.x; xw[4 * u + 1] = X.y; xw[4 * u + 2] = X.z; xw[4 * u + 3] = X.w;
+        yw[4 * u] = Y.x; yw[4 * u + 1] = Y.y; yw[4 * u + 2] = Y.z; yw[4 * u + 3] = Y.w;
+      }
+#pragma unroll
+      for (int e = 0; e < ELEMS; e += 2) {
+        uint32_t xa[EW], ya[EW], xb[EW], yb[EW];
+#pragma unroll
+        for (int i = 0; i < EW; i++) {
+          const int oa = e * Q + 32 * i, ob = (e + 1) * Q + 32 * i;
+          const int wa = oa >> 5, sa = oa & 31, wb = ob >> 5, sb = ob & 31;
+          const uint32_t xa1 = wa + 1 < WORDS ? xw[wa + 1] : 0u, ya1 = wa + 1 < WORDS ? yw[wa + 1] : 0u;
+          const uint32_t xb1 = wb + 1 < WORDS ? xw[wb + 1] : 0u, yb1 = wb + 1 < WORDS ? yw[wb + 1] : 0u;
+          xa[i] = sa ? __funnelshift_r(xw[wa], xa1, sa) : xw[wa];
+          ya[i] = sa ? __funnelshift_r(yw[wa], ya1, sa) : yw[wa];
+          xb[i] = sb ? __funnelshift_r(xw[wb], xb1, sb) : xw[wb];
+          yb[i] = sb ? __funnelshift_r(yw[wb], yb1, sb) : yw[wb];
+        }
+        if constexpr (Q % 32) {
+          constexpr uint32_t m = (1u << (Q % 32)) - 1u;
+          xa[EW - 1] &= m; ya[EW - 1] &= m; xb[EW - 1] &= m; yb[EW - 1] &= m;
+        }
+        acc.add2(xa, ya, xb, yb);
+      }
+    }
+    z = reduce<Q>(acc.unreduced());
+  }
+  // the warp's 32 blocks own output words [first*Q/32, first*Q/32 + Q)
+  uint32_t* so = sout[warp];
+  for (int i = lane; i <= Q; i += 32) so[i] = 0u;
+  __syncwarp();
+  if (l < a.nblocks) {
+    const int bit = lane * Q, w0 = bit >> 5, sh = bit & 31;
+#pragma unroll
+    for (int i = 0; i <= EW; i++) {
+      const uint32_t lo = at(z, i - 1), hi = at(z, i);
+      const uint32_t v = sh ? __funnelshift_l(lo, hi, sh) : hi;
+      if (v) atomicOr(&so[w0 + i], v);
+    }
+  }
+  __syncwarp();
+  const int64_t first = l - lane;
+  if (first < a.nblocks) {
+    const int64_t nv = (a.nblocks - first) < 32 ? (a.nblocks - first) : 32;
+    const int64_t bits = nv * Q;
+    const int words = (int)((bits + 31) >> 5);
+    for (int i = lane; i < words; i += 32) {
+      const int64_t gw = first / 32 * Q + i;
+      BX_CHECK(gw, a.out_words, 8);
+      if ((int64_t)(i + 1) * 32 <= bits) {
+        a.out[gw] = so[i];
+      } else {
+        const uint32_t mask = (1u << (bits & 31)) - 1u;
+        atomicAnd(&a.out[gw], ~mask);
+        atomicOr(&a.out[gw], so[i] & mask);
+      }
+    }
+  }
+}
+
 }  // namespace bx

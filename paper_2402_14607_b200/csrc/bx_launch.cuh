@@ -25,8 +25,20 @@ struct LaunchCfg {
   int units = 0;      // direct: 128-bit units per block
 };
 
+inline bool period_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BX_PERIOD");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+// q with an aligned one-thread-per-block kernel: powers of two
+// (eq_direct_kernel) and q = 24, 40, 48, 56 (eq_period_kernel; BX_PERIOD=0
+// sends those to the TMA kernel, for A/B runs)
 inline bool direct_q(int q) {
-  return q == 1 || q == 2 || q == 4 || q == 8 || q == 16 || q == 32 || q == 64 || q == 128;
+  return q == 1 || q == 2 || q == 4 || q == 8 || q == 16 || q == 32 || q == 64 || q == 128 ||
+         (period_q(q) && period_enabled());
 }
 
 // Aligned fast path eligibility (see eq_direct_kernel).
@@ -215,7 +227,8 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
     return cudaGetLastError();
 #endif
   }
-  if constexpr (Q == 1 || Q == 2 || Q == 4 || Q == 8 || Q == 16 || Q == 32 || Q == 64 || Q == 128) {
+  if constexpr (Q == 1 || Q == 2 || Q == 4 || Q == 8 || Q == 16 || Q == 32 || Q == 64 || Q == 128 ||
+                period_q(Q)) {
     if (c.direct) {
       DirectArgs d;
       d.x = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a.x) + a.x_bit0 / 8);
@@ -241,6 +254,7 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
       attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
+      if constexpr (period_q(Q)) return cudaLaunchKernelEx(&cfg, eq_period_kernel<Q>, d);
       switch (c.units) {
         case 1: return cudaLaunchKernelEx(&cfg, eq_direct_kernel<Q, 1>, d);
         case 2: return cudaLaunchKernelEx(&cfg, eq_direct_kernel<Q, 2>, d);
@@ -249,6 +263,10 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
         default: return cudaLaunchKernelEx(&cfg, eq_direct_kernel<Q, 0>, d);
       }
 #else
+      if constexpr (period_q(Q)) {
+        eq_period_kernel<Q><<<g, b, 0, s>>>(d);
+        return cudaGetLastError();
+      }
       switch (c.units) {
         case 1: eq_direct_kernel<Q, 1><<<g, b, 0, s>>>(d); break;
         case 2: eq_direct_kernel<Q, 2><<<g, b, 0, s>>>(d); break;

@@ -1,6 +1,9 @@
-"""Child process of test_gpu_direct_variants: parity of the direct kernel under
-the load-width knob in the environment (BX_WIDE is read once per process).
+"""Child process of test_gpu_direct_variants: parity of the aligned one-thread-
+per-block kernels (eq_direct_kernel for powers of two, eq_period_kernel for
+q = 24, 40, 48, 56) under the load-width knob in the environment (BX_WIDE is
+read once per process).
 Prints 'ok <cases>' or raises."""
+import math
 import os
 import pathlib
 import random
@@ -17,8 +20,9 @@ from paper_2402_14607_b200 import _lib, device as D
 def main():
     rnd = random.Random(int(sys.argv[1]) if len(sys.argv) > 1 else 7)
     cases = 0
-    for q in (1, 2, 4, 8, 16, 32, 64, 128):
-        for units in (1, 2, 3, 4, 5, 8, 9, 16):
+    for q in (1, 2, 4, 8, 16, 32, 64, 128, 24, 40, 48, 56):
+        period = q // math.gcd(q, 128)        # 128-bit units per element period
+        for units in (1, 2, 3, 4, 5, 8, 9, 16, period, 2 * period, 3 * period):
             if (128 * units) % q:
                 continue
             n = 128 * units // q
