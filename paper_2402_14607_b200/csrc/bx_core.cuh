@@ -1086,6 +1086,9 @@ __host__ __device__ constexpr bool period_q(int q) {
 #ifndef BX_PERIOD_MINB
 #define BX_PERIOD_MINB 2
 #endif
+#ifndef BX_PERIOD_PAIR
+#define BX_PERIOD_PAIR 1
+#endif
 
 template <int Q>
 __global__ void __launch_bounds__(256, BX_PERIOD_MINB) eq_period_kernel(const DirectArgs a) {
@@ -1134,7 +1137,12 @@ __global__ void __launch_bounds__(256, BX_PERIOD_MINB) eq_period_kernel(const Di
           constexpr uint32_t m = (1u << (Q % 32)) - 1u;
           xa[EW - 1] &= m; ya[EW - 1] &= m; xb[EW - 1] &= m; yb[EW - 1] &= m;
         }
+#if BX_PERIOD_PAIR
         acc.add2(xa, ya, xb, yb);
+#else
+        acc.add(xa, ya);
+        acc.add(xb, yb);
+#endif
       }
     }
     z = reduce<Q>(acc.unreduced());
