@@ -325,7 +325,7 @@ def run_ours(args, wl) -> None:
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "kernel_ms": ms_step, "launch": _lib.launch_info(wl.q, wl.n, nblocks)}
     li = roofline["launch"]
-    pow2 = wl.q & (wl.q - 1) == 0
+    pow2 = (wl.q & (wl.q - 1)) == 0
     roofline["kernel"] = (f"bx::eq_direct_kernel<{wl.q}, {u if (u := wl.block_bits // 128) in (1, 2, 4, 8) else 0}>"
                           if li["direct"] and pow2
                           else f"bx::eq_period_kernel<{wl.q}>" if li["direct"]
