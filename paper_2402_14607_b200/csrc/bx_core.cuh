@@ -1084,20 +1084,24 @@ __host__ __device__ constexpr bool period_q(int q) {
 }
 
 #ifndef BX_PERIOD_MINB
-#define BX_PERIOD_MINB 2
+#define BX_PERIOD_MINB 4
 #endif
 #ifndef BX_PERIOD_PAIR
 #define BX_PERIOD_PAIR 1
 #endif
 
+#ifndef BX_PERIOD_THREADS
+#define BX_PERIOD_THREADS 128
+#endif
+
 template <int Q>
-__global__ void __launch_bounds__(256, BX_PERIOD_MINB) eq_period_kernel(const DirectArgs a) {
+__global__ void __launch_bounds__(BX_PERIOD_THREADS, BX_PERIOD_MINB) eq_period_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int G = cgcd(Q, 128);
   constexpr int UNITS = Q / G;          // 128-bit units per period
   constexpr int ELEMS = 128 / G;        // elements per period (even)
   constexpr int WORDS = 4 * UNITS;
-  __shared__ uint32_t sout[8][Q + 1];
+  __shared__ uint32_t sout[BX_PERIOD_THREADS / 32][Q + 1];
   pdl_entry();
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
