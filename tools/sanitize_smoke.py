@@ -20,7 +20,8 @@ rnd = random.Random(3)
 fails = 0
 cases = [(4, 64, 700, 0), (2, 64, 300, 0), (8, 64, 129, 0), (16, 64, 77, 0), (32, 64, 40, 0),
          (64, 8, 55, 0), (128, 8, 33, 0), (56, 48, 45, 3), (58, 120, 17, 5), (80, 71, 9, 0),
-         (13, 7, 300, 11), (1, 24, 500, 1), (3, 50, 90, 0), (127, 3, 40, 9), (100, 2000, 3, 0)]
+         (13, 7, 300, 11), (1, 24, 500, 1), (3, 50, 90, 0), (127, 3, 40, 9), (100, 2000, 3, 0),
+         (56, 48, 45, 0), (24, 16, 70, 0), (40, 32, 33, 0), (48, 8, 65, 0)]   # period kernel
 for q, n, k, off in cases:
     nb = (off + k * q * n + 7) // 8
     xb, yb = rnd.randbytes(nb), rnd.randbytes(nb)
