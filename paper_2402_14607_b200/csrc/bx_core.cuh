@@ -989,8 +989,17 @@ __device__ __forceinline__ Wide<8> direct_block_q128(const uint4* xp, const uint
 #define BX_DIRECT_MINB_Q128(U) ((U) == 0 || (U) >= 8 ? 3 : 2)
 #endif
 
+// CTA size of the direct kernel: 128 threads (twice the CTAs per SM, same
+// registers) for q >= 32, where it gains 3% (q = 32, 128); 256 below, where
+// blocks are small and 128-thread CTAs hit the CTA launch rate (q = 2: -42%)
+// -- profiles/r01_direct_sweep.txt O.
+__host__ __device__ constexpr int direct_threads(int q) { return q >= 32 ? 128 : 256; }
+
 template <int Q, int U>
-__global__ void __launch_bounds__(256, (Q == 128 ? BX_DIRECT_MINB_Q128(U) : (Q > 32 ? 2 : (Q > 16 ? BX_DIRECT_MINB_Q32 : 1))))
+__global__ void __launch_bounds__(direct_threads(Q),
+                                  (256 / direct_threads(Q)) *
+                                      (Q == 128 ? BX_DIRECT_MINB_Q128(U)
+                                                : (Q > 32 ? 2 : (Q > 16 ? BX_DIRECT_MINB_Q32 : 1))))
     eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);

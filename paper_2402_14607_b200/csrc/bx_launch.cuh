@@ -106,7 +106,7 @@ inline LaunchCfg choose_direct(int q, int n, int64_t nblocks) {
   c.direct = 1;
   c.tpb_log2 = 0;
   // small runs: narrower CTAs so the blocks spread over more SMs
-  int threads = period_q(q) ? BX_PERIOD_THREADS : 256;
+  int threads = period_q(q) ? BX_PERIOD_THREADS : direct_threads(q);
   while (threads > 64 && (nblocks + threads - 1) / threads < 2 * (int64_t)sm_count()) threads /= 2;
   c.tile = threads;
   c.threads = threads;
