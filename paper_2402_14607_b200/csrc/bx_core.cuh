@@ -940,14 +940,23 @@ __device__ __forceinline__ void q128_part(const uint4& v, uint32_t (&o)[2]) {
 }
 
 template <int P>
-__device__ __forceinline__ void q128_pass(const uint4* xp, const uint4* yp, int units, Wide<8>& c) {
+__device__ __forceinline__ void q128_pass(const uint4* xp, const uint4* yp, int units, bool wide,
+                                          Wide<8>& c) {
   Holes<64> acc;
   acc.init();
   int u = 0;
 #pragma unroll 1
   for (; u + 1 < units; u += 2) {
-    const uint4 X0 = __ldg(xp + u), Y0 = __ldg(yp + u);
-    const uint4 X1 = __ldg(xp + u + 1), Y1 = __ldg(yp + u + 1);
+    uint4 X0, X1, Y0, Y1;
+    if (wide) {            // the passes re-read the block: halve the L1 requests
+      ldg256(xp + u, X0, X1);
+      ldg256(yp + u, Y0, Y1);
+    } else {
+      X0 = __ldg(xp + u);
+      Y0 = __ldg(yp + u);
+      X1 = __ldg(xp + u + 1);
+      Y1 = __ldg(yp + u + 1);
+    }
     uint32_t a[2], b[2], a2[2], b2[2];
     q128_part<P>(X0, a);
     q128_part<P>(Y0, b);
@@ -970,11 +979,12 @@ __device__ __forceinline__ void q128_pass(const uint4* xp, const uint4* yp, int 
   }
 }
 
-__device__ __forceinline__ Wide<8> direct_block_q128(const uint4* xp, const uint4* yp, int units) {
+__device__ __forceinline__ Wide<8> direct_block_q128(const uint4* xp, const uint4* yp, int units,
+                                                     bool wide) {
   Wide<8> c = wzero<8>();
-  q128_pass<0>(xp, yp, units, c);
-  q128_pass<1>(xp, yp, units, c);
-  q128_pass<2>(xp, yp, units, c);
+  q128_pass<0>(xp, yp, units, wide, c);
+  q128_pass<1>(xp, yp, units, wide, c);
+  q128_pass<2>(xp, yp, units, wide, c);
   return c;
 }
 
@@ -1027,7 +1037,7 @@ __global__ void __launch_bounds__(direct_threads(Q),
         c.w[0] = acc.unreduced();
       } else {
         if constexpr (Q == 128 && BX_Q128_PASSES) {
-          c = direct_block_q128(xp, yp, units);
+          c = direct_block_q128(xp, yp, units, a.wide);
         } else {
           Holes<Q> acc;
           acc.init();

@@ -49,7 +49,7 @@ inline bool direct_ok(int q, int n, int64_t x_bit0, int64_t y_bit0, int64_t out_
          out_bit0 % 32 == 0 && (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
 }
 
-// 256-bit loads in the q = 16 direct kernel (BX_WIDE=0 disables, for A/B runs).
+// 256-bit loads in the q = 16 and q = 128 direct kernels (BX_WIDE=0 disables, for A/B runs).
 inline bool wide_loads_enabled() {
   static const bool on = [] {
     const char* e = getenv("BX_WIDE");
@@ -236,7 +236,7 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
       d.nblocks = a.nblocks;
       d.out = a.out + a.out_bit0 / 32;
       d.units = c.units;
-      d.wide = (Q == 16 && c.units % 2 == 0 && wide_loads_enabled() &&
+      d.wide = ((Q == 16 || Q == 128) && c.units % 2 == 0 && wide_loads_enabled() &&
                 ((reinterpret_cast<uintptr_t>(d.x) | reinterpret_cast<uintptr_t>(d.y)) & 31) == 0)
                    ? 1 : 0;
       d.x_limit = a.x_limit / 4 - a.x_bit0 / 128;
