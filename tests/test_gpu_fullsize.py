@@ -3,7 +3,8 @@
 * config 2 (c2) in full: reference-identical seeded streams (pinned by
   tests/golden/streams.json), every block vs the CPU oracle, plus the
   reference's own outputs at sampled blocks (tests/golden/sampled.json);
-* config 3 (c3) and the planner shapes: sampled reference blocks;
+* configs 3, 4, the planner shapes, paper and c5 (first 2^33 bits) in full vs
+  the oracle; config 3 and the planner shapes also at sampled reference blocks;
 * size-independent properties at full size: bilinearity
   E(x1^x2, y) = E(x1, y) ^ E(x2, y), zero annihilation, segmentation and
   device-sharding invariance.
@@ -66,6 +67,23 @@ def test_sampled_reference_blocks_full_size(golden, name):
             assert _block(got, l, wl.q) == int(z, 16), (name, l)
             checked += 1
     assert checked >= 3
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c2p", "c4p", "paper", "c5_n1024", "c5_n2048"])
+def test_full_output_vs_oracle(name):
+    """Every block of the config (c5: the first 2^33 bits of each stream) against
+    the CPU oracle (PCLMUL mode, all host threads), so each kernel family's
+    full-size launch -- the one bench.py times -- is bit-exact end to end."""
+    wl = W.WORKLOADS[name]
+    samples = wl.samples if not name.startswith("c5") else (2**33) // wl.b
+    xd, nbytes = W.stream_device(wl.x, samples)
+    yd, _ = W.stream_device(wl.y, samples)
+    nblocks = samples * wl.b // wl.block_bits
+    got = _run(xd, yd, nbytes, wl, nblocks).cpu().numpy().tobytes()
+    xh = xd[:nbytes].cpu().numpy()
+    yh = yd[:nbytes].cpu().numpy()
+    del xd, yd
+    assert got == coracle.extract_eq(xh, yh, wl.q, wl.n, nblocks), name
 
 
 @pytest.mark.parametrize("q,n", [(4, 64), (4, 128), (2, 64), (8, 64), (16, 64), (32, 64),
