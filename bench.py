@@ -38,6 +38,12 @@ import sys
 import threading
 import time
 
+if "RANK" in os.environ and os.environ.get("NCCL_DEBUG") == "VERSION":
+    # under torchrun: keep stdout to the one JSON line -- with NCCL_DEBUG set
+    # (the image sets VERSION) NCCL prints a version banner on stdout at
+    # communicator init; a debug level the caller chose (INFO, ...) is kept
+    del os.environ["NCCL_DEBUG"]
+
 REPO = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
