@@ -253,8 +253,17 @@ class _Source:
             self._total = len(self._mem)
         elif hasattr(stream, "read"):
             self._file = stream
-            self._parts = bytearray()
-            self._parts_base = 0      # stream byte offset of _parts[0]
+            # delivered bytes live in one numpy buffer: [_start, _start + _len)
+            # holds stream bytes [_parts_base, _parts_base + _len).  Standard
+            # io readers fill it in place with readinto (same call sizes and
+            # semantics as read(size)); other objects go through read().
+            self._buf = None
+            self._start = 0
+            self._len = 0
+            self._parts_base = 0
+            self._readinto = isinstance(stream, (io.BufferedIOBase, io.RawIOBase)) and \
+                hasattr(stream, "readinto")
+            self._size_hint = self.known_bytes()
         else:
             raise TypeError(f"cannot read from {type(stream).__name__}")
         self.buffered = 0             # bytes delivered by read() so far
@@ -277,14 +286,44 @@ class _Source:
         except (AttributeError, OSError, ValueError, io.UnsupportedOperation):
             return None
 
+    #: largest buffer allocated up front from a regular file's size; beyond it
+    #: the buffer grows geometrically (consumed bytes are released per segment)
+    PREALLOC_MAX = 1 << 30
+
+    def _reserve(self, need: int) -> None:
+        """Room for `need` more bytes after the held ones (amortised O(1):
+        compaction or geometric growth, never a copy per read)."""
+        cap = 0 if self._buf is None else self._buf.size
+        end = self._start + self._len
+        if end + need <= cap:
+            return
+        if self._len + need <= cap and self._start >= self._len:
+            # compact: the released prefix is at least as large as the live data
+            self._buf[:self._len] = self._buf[self._start:end]
+            self._start = 0
+            return
+        first = self._size_hint if (self._buf is None and self._size_hint) else 0
+        new_cap = max(self._len + need, 2 * cap, min(first, self.PREALLOC_MAX), 1 << 20)
+        buf = np.empty(new_cap, dtype=np.uint8)
+        if self._len:
+            buf[:self._len] = self._buf[self._start:end]
+        self._buf, self._start = buf, 0
+
     def _read(self, need: int) -> int:
         if self._mem is not None:
             got = min(need, self._total - self.buffered)
             return max(got, 0)
-        data = self._file.read(need)
-        if data:
-            self._parts += data
-        return len(data) if data else 0
+        self._reserve(need)
+        end = self._start + self._len
+        if self._readinto:
+            got = self._file.readinto(memoryview(self._buf)[end:end + need]) or 0
+        else:
+            data = self._file.read(need)
+            got = len(data) if data else 0
+            if got:
+                self._buf[end:end + got] = np.frombuffer(data, dtype=np.uint8)
+        self._len += got
+        return got
 
     def fill(self, want_bits: int) -> None:
         while self.avail() < want_bits and not self.exhausted:
@@ -326,15 +365,16 @@ class _Source:
         """Stream bytes [byte_lo, byte_hi) (all already delivered)."""
         if self._mem is not None:
             return self._mem[byte_lo:byte_hi]
-        lo = byte_lo - self._parts_base
-        return memoryview(self._parts)[lo:byte_hi - self._parts_base]
+        lo = self._start + byte_lo - self._parts_base
+        return memoryview(self._buf)[lo:lo + byte_hi - byte_lo]
 
     def release(self, byte_lo: int) -> None:
         """Forget buffered file bytes before stream offset byte_lo."""
         if self._file is not None and byte_lo > self._parts_base:
-            cut = byte_lo - self._parts_base
-            del self._parts[:cut]
-            self._parts_base = byte_lo
+            cut = min(byte_lo - self._parts_base, self._len)
+            self._start += cut
+            self._len -= cut
+            self._parts_base += cut
 
 
 # ------------------------------------------------------------- extraction

@@ -77,7 +77,10 @@ def test_launch_info_geometry():
             assert li["threads"] == li["tpb"] * li["tile"]
             assert li["threads"] % 32 == 0 and li["threads"] <= 256
             assert li["family"] == ("diag" if q <= 8 else "holes")
-            assert li["direct"] == (q in (1, 2, 4, 8, 16, 32, 64, 128) and q * n % 128 == 0)
+            # one-thread-per-block kernels: eq_direct_kernel (powers of two) and
+            # eq_period_kernel (q = 24, 40, 48, 56), for 128-bit-aligned blocks
+            assert li["direct"] == (q in (1, 2, 4, 8, 16, 32, 64, 128, 24, 40, 48, 56)
+                                    and q * n % 128 == 0)
             ntiles = -(-10_000 // li["tile"])
             if li["tma"]:
                 assert 0 < li["grid"] <= ntiles and li["staged"]
