@@ -258,6 +258,7 @@ class _Source:
             # io readers fill it in place with readinto (same call sizes and
             # semantics as read(size)); other objects go through read().
             self._buf = None
+            self._keep = None         # owner of _buf when it is a pinned tensor
             self._start = 0
             self._len = 0
             self._parts_base = 0
@@ -304,10 +305,24 @@ class _Source:
             return
         first = self._size_hint if (self._buf is None and self._size_hint) else 0
         new_cap = max(self._len + need, 2 * cap, min(first, self.PREALLOC_MAX), 1 << 20)
-        buf = np.empty(new_cap, dtype=np.uint8)
+        buf, keep = self._host_buffer(new_cap)
         if self._len:
             buf[:self._len] = self._buf[self._start:end]
-        self._buf, self._start = buf, 0
+        self._buf, self._keep, self._start = buf, keep, 0
+
+    @staticmethod
+    def _host_buffer(nbytes: int):
+        """Pinned host memory when CUDA is up (pre-faulted, reused through
+        torch's host allocator cache, and the chunks' H2D then goes straight
+        from it without staging copies); plain numpy memory otherwise."""
+        try:
+            import torch
+            if torch.cuda.is_available():
+                t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+                return t.numpy(), t
+        except (ImportError, RuntimeError):  # pragma: no cover - no CUDA runtime
+            pass
+        return np.empty(nbytes, dtype=np.uint8), None
 
     def _read(self, need: int) -> int:
         if self._mem is not None:
