@@ -19,6 +19,7 @@ device memory on long or unbounded inputs.
 from __future__ import annotations
 
 import io
+import mmap
 import os
 import stat
 import time
@@ -251,6 +252,8 @@ class _Source:
         elif isinstance(stream, (bytes, bytearray, memoryview)):
             self._mem = memoryview(stream).cast("B")
             self._total = len(self._mem)
+        elif self._map_file(stream):
+            pass
         elif hasattr(stream, "read"):
             self._file = stream
             # delivered bytes live in one numpy buffer: [_start, _start + _len)
@@ -270,6 +273,39 @@ class _Source:
         self.buffered = 0             # bytes delivered by read() so far
         self.consumed = 0             # bits handed out (BitReader.bits_consumed)
         self.exhausted = False
+
+    #: regular files at least this large are memory-mapped (smaller ones are read)
+    MAP_MIN_BYTES = 1 << 20
+
+    def _map_file(self, stream) -> bool:
+        """Regular binary files are mapped read-only (page cache, no read()
+        copies) and replayed like in-memory bytes; reads of a regular file
+        return min(size, remaining) bytes, so the closed-form BitReader replay
+        holds, and the file's position is kept where the reference's read()
+        calls would have left it (_sync_pos)."""
+        if not isinstance(stream, (io.BufferedReader, io.FileIO)):
+            return False
+        self._pos_file = None
+        try:
+            fd = stream.fileno()
+            st = os.fstat(fd)
+            if not stat.S_ISREG(st.st_mode):
+                return False
+            pos = stream.tell()
+            if st.st_size - pos < self.MAP_MIN_BYTES:
+                return False
+            flags = mmap.MAP_SHARED | getattr(mmap, "MAP_POPULATE", 0)
+            self._map = mmap.mmap(fd, st.st_size, flags=flags, prot=mmap.PROT_READ)
+        except (AttributeError, OSError, ValueError, io.UnsupportedOperation):
+            return False
+        self._mem = memoryview(self._map)[pos:]
+        self._total = st.st_size - pos
+        self._pos_file, self._pos0 = stream, pos
+        return True
+
+    def _sync_pos(self) -> None:
+        if getattr(self, "_pos_file", None) is not None:
+            self._pos_file.seek(self._pos0 + self.buffered)
 
     def avail(self) -> int:
         return self.buffered * 8 - self.consumed
@@ -348,6 +384,7 @@ class _Source:
                 self.exhausted = True
                 break
             self.buffered += got
+        self._sync_pos()
 
     def take(self, nbits: int) -> bool:
         """read_bits(nbits): False (nothing consumed) if fewer bits remain."""
@@ -375,6 +412,7 @@ class _Source:
         self.consumed += k * B
         reads = -(-self.consumed // (8 * READ_CHUNK))
         self.buffered = max(self.buffered, min(self._total, reads * READ_CHUNK))
+        self._sync_pos()
 
     def window(self, byte_lo: int, byte_hi: int):
         """Stream bytes [byte_lo, byte_hi) (all already delivered)."""

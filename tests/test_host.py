@@ -139,6 +139,32 @@ def test_eq_reports_file_streams(golden, oracle_compute):
                 assert report_dict(rep) == c["report"], c["tag"]
 
 
+def test_eq_reports_mapped_files(golden, oracle_compute, tmp_path, monkeypatch):
+    """Regular files are memory-mapped and replayed in closed form: same bytes
+    and report as the reference, and each file is left at the position the
+    reference's read() calls would have left it (as a BytesIO source shows)."""
+    from paper_2402_14607_b200 import extractor as E
+    monkeypatch.setattr(E._Source, "MAP_MIN_BYTES", 0)
+    for c in golden("eq_cases.json")[-12:]:
+        xb, yb = case_inputs(c)
+        if not xb or not yb:
+            continue
+        plan = tiny_eq_plan(bx, c["b"], c["samples"], c.get("rate", "3/4"), c["n"], c["q"])
+        bx_, by_ = io.BytesIO(xb), io.BytesIO(yb)
+        bx.extract_eq(bx_, by_, plan, max_blocks=c.get("max_blocks")).run(io.BytesIO())
+        (tmp_path / "x").write_bytes(b"HDR" + xb)
+        (tmp_path / "y").write_bytes(yb)
+        with open(tmp_path / "x", "rb") as fx, open(tmp_path / "y", "rb") as fy:
+            fx.read(3)                               # start mid-file
+            run = bx.extract_eq(fx, fy, plan, max_blocks=c.get("max_blocks"))
+            assert run._x._pos_file is fx           # the mapped path is the one under test
+            sink = io.BytesIO()
+            rep = run.run(sink)
+            assert sink.getvalue().hex() == c["out"], c["tag"]
+            assert report_dict(rep) == c["report"], c["tag"]
+            assert (fx.tell() - 3, fy.tell()) == (bx_.tell(), by_.tell()), c["tag"]
+
+
 def test_neq_reports_match_reference(golden, oracle_compute):
     for c in golden("neq_cases.json"):
         if c.get("zeros"):
