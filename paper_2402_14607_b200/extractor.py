@@ -235,7 +235,7 @@ class _Source:
     are kept until the blocks that use them are computed.
     """
 
-    def __init__(self, stream):
+    def __init__(self, stream, allow_map: bool = True):
         self._mem = None
         self._file = None
         try:
@@ -252,7 +252,7 @@ class _Source:
         elif isinstance(stream, (bytes, bytearray, memoryview)):
             self._mem = memoryview(stream).cast("B")
             self._total = len(self._mem)
-        elif self._map_file(stream):
+        elif allow_map and self._map_file(stream):
             pass
         elif hasattr(stream, "read"):
             self._file = stream
@@ -444,8 +444,11 @@ class Extraction:
     def __init__(self, x_stream, y_stream, plan, *, workers: int = 1,
                  max_blocks: int | None = None, device=None, devices=None,
                  segment_blocks: int = DEFAULT_SEGMENT_BLOCKS):
-        self._x = _Source(x_stream)
-        self._y = _Source(y_stream)
+        # one file object feeding both streams is read alternately (x, y, x,
+        # ...) exactly as the reference does; only distinct objects are mapped
+        shared = x_stream is y_stream
+        self._x = _Source(x_stream, allow_map=not shared)
+        self._y = _Source(y_stream, allow_map=not shared)
         self.plan = plan
         self.mode = "eq" if _params.is_eq_plan(plan) else "neq"
         self._workers = workers

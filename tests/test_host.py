@@ -163,6 +163,18 @@ def test_eq_reports_mapped_files(golden, oracle_compute, tmp_path, monkeypatch):
             assert sink.getvalue().hex() == c["out"], c["tag"]
             assert report_dict(rep) == c["report"], c["tag"]
             assert (fx.tell() - 3, fy.tell()) == (bx_.tell(), by_.tell()), c["tag"]
+    # one file object feeding both streams: read alternately, never mapped
+    c = golden("eq_cases.json")[-1]
+    xb, yb = case_inputs(c)
+    plan = tiny_eq_plan(bx, c["b"], c["samples"], c.get("rate", "3/4"), c["n"], c["q"])
+    both = io.BytesIO(xb + yb)
+    want = bx.extract_eq(both, both, plan).run(io.BytesIO())
+    (tmp_path / "xy").write_bytes(xb + yb)
+    with open(tmp_path / "xy", "rb") as f:
+        run = bx.extract_eq(f, f, plan)
+        assert run._x._mem is None
+        assert report_dict(run.run(io.BytesIO())) == report_dict(want)
+        assert f.tell() == both.tell()
 
 
 def test_neq_reports_match_reference(golden, oracle_compute):
