@@ -188,8 +188,16 @@ __device__ __forceinline__ uint32_t read32(const uint32_t* src, T off, int64_t l
 
 // ------------------------------------------------------------- diag (Q<=8)
 
+// Merged diagonal accumulators (explicit LOP3s) for q = 4: c2 +3.5%, c5 n=256
+// +5%; q = 8 loses 13% (two dependent LOP3s per accumulator and word), q = 2
+// 1% -- profiles/r01_direct_sweep.txt R.  BX_DIAG_MERGED=0 turns it off.
+#ifndef BX_DIAG_MERGED
+#define BX_DIAG_MERGED 1
+#endif
+
 template <int Q>
 struct Diag {
+  static constexpr bool kMerged = BX_DIAG_MERGED && Q == 4;
   static constexpr int E = 32 / Q;   // elements per 32-bit chunk
   static constexpr int EB = E * Q;   // bits per chunk
   // acc(d) is the sum of the two diagonals at distance d:
@@ -210,13 +218,27 @@ struct Diag {
   }
 
   __device__ __forceinline__ void add(uint32_t X, uint32_t Y) {
+    if constexpr (kMerged) {
+      // one accumulator per d, updated by two explicit a ^ (b & c) LOP3s (ptxas
+      // cannot re-associate inline lop3 into AND/XOR trees): the same 2Q-1 LOP3
+      // per word pair, Q-1 fewer registers, no pos ^ neg merge per block
 #pragma unroll
-    for (int d = 0; d < Q; d++) pos[d] ^= X & (Y << d);
+      for (int d = 0; d < Q; d++) {
+        asm("lop3.b32 %0, %0, %1, %2, 0x78;" : "+r"(pos[d]) : "r"(X), "r"(Y << d));
+        if (d) asm("lop3.b32 %0, %0, %1, %2, 0x78;" : "+r"(pos[d]) : "r"(X << d), "r"(Y));
+      }
+    } else {
 #pragma unroll
-    for (int d = 1; d < Q; d++) neg[d] ^= (X << d) & Y;
+      for (int d = 0; d < Q; d++) pos[d] ^= X & (Y << d);
+#pragma unroll
+      for (int d = 1; d < Q; d++) neg[d] ^= (X << d) & Y;
+    }
   }
 
-  __device__ __forceinline__ uint32_t acc(int d) const { return d ? pos[d] ^ neg[d] : pos[0]; }
+  __device__ __forceinline__ uint32_t acc(int d) const {
+    if constexpr (kMerged) return pos[d];
+    else return d ? pos[d] ^ neg[d] : pos[0];
+  }
 
   static __host__ __device__ constexpr uint32_t mask_b(int b) {   // bit b of every element
     uint32_t m = 0;
