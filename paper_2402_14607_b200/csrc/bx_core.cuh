@@ -1047,7 +1047,7 @@ __global__ void __launch_bounds__(direct_threads(Q),
     // U > 0: the unit count is a compile-time constant (fully unrolled,
     // all loads issued up front); U == 0: runtime count.
     const int units = U > 0 ? U : a.units;
-    if (Q == 16 && a.wide) {
+    if (Q <= 16 && a.wide) {
       z = reduce<Q>(direct_block_wide<Q>(xp, yp, units));
     } else {
       Wide<CW> c;

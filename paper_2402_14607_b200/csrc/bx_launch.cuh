@@ -236,7 +236,11 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
       d.nblocks = a.nblocks;
       d.out = a.out + a.out_bit0 / 32;
       d.units = c.units;
-      d.wide = ((Q == 16 || Q == 128) && c.units % 2 == 0 && wide_loads_enabled() &&
+      // 256-bit loads (two units per load; sweeps C, P, T): q = 8, 16, 128 at
+      // any even unit count; q <= 4 from 8 units per block up (the fully
+      // unrolled 128-bit form of those is register-bound: q=4 n=256 +57%)
+      d.wide = ((Q == 8 || Q == 16 || Q == 128 || (Q <= 4 && c.units >= 8)) && c.units % 2 == 0 &&
+                wide_loads_enabled() &&
                 ((reinterpret_cast<uintptr_t>(d.x) | reinterpret_cast<uintptr_t>(d.y)) & 31) == 0)
                    ? 1 : 0;
       d.x_limit = a.x_limit / 4 - a.x_bit0 / 128;
