@@ -222,6 +222,35 @@ def test_host_pipeline_chunking(monkeypatch):
         monkeypatch.setattr(sharding, "PIPE_CHUNK_BYTES", 64 << 20)
 
 
+def test_mapped_file_inputs(tmp_path):
+    """Regular files >= 1 MiB take the memory-mapped path: output equals the
+    oracle, and with max_blocks the files stop where the reference's 64 KiB
+    reads would leave them (as BytesIO sources of the same bytes do)."""
+    rnd = random.Random(23)
+    q, n = 56, 48
+    k = 4000                                  # 1.34 MB per stream (>= the 1 MiB map threshold)
+    nb = k * q * n // 8 + 5000
+    xb, yb = rnd.randbytes(nb), rnd.randbytes(nb)
+    (tmp_path / "x").write_bytes(xb)
+    (tmp_path / "y").write_bytes(yb)
+    plan = tiny_eq_plan(bx, 8, nb, "3/4", n, q)
+    full = plan.num_blocks
+    want = coracle.extract_eq(xb, yb, q, n, full)
+    for limit in (None, 777):
+        with open(tmp_path / "x", "rb") as fx, open(tmp_path / "y", "rb") as fy:
+            run = bx.extract_eq(fx, fy, plan, max_blocks=limit)
+            assert run._x._pos_file is fx
+            sink = io.BytesIO()
+            rep = run.run(sink)
+            m = full if limit is None else limit
+            got = int.from_bytes(sink.getvalue(), "little")
+            assert got == int.from_bytes(want, "little") & ((1 << (m * q)) - 1)
+            bxio, byio = io.BytesIO(xb), io.BytesIO(yb)
+            rep2 = bx.extract_eq(bxio, byio, plan, max_blocks=limit).run(io.BytesIO())
+            assert report_dict(rep) == report_dict(rep2)
+            assert (fx.tell(), fy.tell()) == (bxio.tell(), byio.tell())
+
+
 def test_pack_kats(golden):
     for c in golden("pack.json"):
         vals = np.array([int(v, 16) for v in c["values"]], dtype=np.uint64)
