@@ -143,8 +143,9 @@ WORKLOADS: dict[str, Workload] = {
     "c5_n512": _c5(512),
     "c5_n1024": _c5(1024),
     "c5_n2048": _c5(2048),
-    "paper": Workload("paper", 80, 71, 2**24, uniform8_spec(1), uniform8_spec(2),
-                      note="paper flagship shape q=80, n=71 (PAPER.md:268-270)"),
+    "paper": Workload("paper", 80, 71, 2**28, uniform8_spec(1), uniform8_spec(2),
+                      note="paper flagship shape q=80, n=71 (PAPER.md:268-270); 2x256 MiB "
+                           "streams like config 2 (a steady-state stream, larger than L2)"),
 }
 
 
