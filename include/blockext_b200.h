@@ -53,14 +53,16 @@ int bx_modulus_exponents(int q, int* exps);
  * preserved (boundary words are updated atomically).
  *
  * x, y, out: device pointers, 4-byte aligned; the kernels run on the device
- * that owns x, and out may be memory of a peer GPU mapped into this process
+ * of `stream` (non-NULL) or else the device that owns x -- never out's: out may
+ * be memory of a peer GPU mapped into this process
  * (CUDA IPC / peer access: the outputs are then stored over NVLink -- how
  * sharding.distributed_extract(gather="peer") gathers ranks' ranges into rank
  * 0's buffer).  x_bytes / y_bytes: bytes of
  * valid stream data; the buffers must stay readable up to round_up(x_bytes, 16)
  * + 16 bytes (the TMA-bulk path copies whole 16-byte granules).  16-byte
  * aligned x and y select the aligned kernels (direct, or persistent TMA-bulk).
- * Requires x_bit0 + nblocks*q*n <= 8*x_bytes (same for y).
+ * Requires x_bit0 + nblocks*q*n <= 8*x_bytes (same for y).  y and out must be
+ * local to the compute device or on a peer it can access (else BX_EINVAL).
  */
 int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0,
                   const void* y, int64_t y_bytes, int64_t y_bit0,
@@ -179,7 +181,8 @@ int bx_rows_uniform(const void* counts, uint32_t nrows, uint32_t bins, uint32_t 
  * returns -1 in normal builds. */
 int64_t bx_checked_violations(int reset, int64_t* first);
 
-/* Number of kernel launches issued by this thread since the last reset. */
+/* Number of kernel launches issued by this process (all threads, all devices)
+ * since the last reset (reset != 0 returns the count and zeroes it). */
 int64_t bx_launch_count(int reset);
 
 #ifdef __cplusplus

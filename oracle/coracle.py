@@ -76,6 +76,8 @@ def extract_eq(x, y, q: int, n: int, nblocks: int, *, x_bit0: int = 0, y_bit0: i
     """Packed output bytes of `nblocks` equal-width blocks.
 
     mode 0 = literal reference algorithm (reduce every product), mode 1 = PCLMUL
+    unreduced accumulation, mode 2 = mode 1 with byte-table / whole-element loads for
+    byte-aligned q in {1,2,4,8,16,32,64} (bulk whole-stream checks);
     unreduced accumulation; both are pinned to the reference fixtures.
     """
     xa, xp = _buf(x)

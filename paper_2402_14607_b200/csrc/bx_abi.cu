@@ -52,24 +52,57 @@ thread_local std::string g_err;
 
 // The library links its own (static) CUDA runtime, whose per-thread current
 // device is independent of the caller's runtime (e.g. torch's).  Every entry
-// point therefore switches to the device that owns its buffers for the
-// duration of the call, so multi-GPU callers (torchrun ranks, per-device
-// threads) launch on the right device with their own streams.
+// point therefore switches, for the duration of the call, to the device the
+// work runs on: the device of the caller's stream when one is given, else the
+// device that owns the call's INPUT (x / samples / counts).  Never the output:
+// an output may be a peer GPU's buffer mapped into this process (CUDA IPC,
+// distributed_extract(gather="peer")), and choosing its device would size the
+// grid for, and launch on, the wrong GPU with a stream that is not its own.
+int device_of(const void* p) {
+  cudaPointerAttributes at;
+  if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) return -1;
+  return at.device;
+}
+
 struct DeviceScope {
   int prev = -1;
-  explicit DeviceScope(const void* p) {
-    cudaPointerAttributes at;
-    if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+  int dev = -1;   // device the call's kernels run on
+  DeviceScope(const void* input, void* stream) {
+    int d = -1;
+    if (stream && cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &d) != cudaSuccess) {
       cudaGetLastError();
-      return;
+      d = -1;
     }
-    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) return;
+    if (d < 0) d = device_of(input);
     int cur = 0;
-    if (cudaGetDevice(&cur) == cudaSuccess && cur != at.device && cudaSetDevice(at.device) == cudaSuccess)
-      prev = cur;
+    if (cudaGetDevice(&cur) != cudaSuccess) cur = 0;
+    dev = d < 0 ? cur : d;
+    if (cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
   }
   ~DeviceScope() {
     if (prev >= 0) cudaSetDevice(prev);
+  }
+  // true if a kernel on `dev` may dereference p: host/unregistered pointers
+  // are left to the caller (UVA host memory), device memory must be local or
+  // on a peer this device can access
+  bool reaches(const void* p) const {
+    const int d = device_of(p);
+    if (d < 0 || d == dev) return true;
+    static int memo[64][64];   // 0 unknown, 1 yes, 2 no
+    if (dev >= 64 || d >= 64) return true;
+    if (!memo[dev][d]) {
+      int ok = 0;
+      if (cudaDeviceCanAccessPeer(&ok, dev, d) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+      }
+      memo[dev][d] = ok ? 1 : 2;
+    }
+    return memo[dev][d] == 1;
   }
   DeviceScope(const DeviceScope&) = delete;
   DeviceScope& operator=(const DeviceScope&) = delete;
@@ -130,7 +163,9 @@ int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0, const void* y,
   if (!x || !y || !out) return fail(BX_EINVAL, "null buffer");
   if (((uintptr_t)x | (uintptr_t)y | (uintptr_t)out) & 3)
     return fail(BX_EINVAL, "buffers must be 4-byte aligned");
-  const DeviceScope scope(out);
+  const DeviceScope scope(x, stream);
+  if (!scope.reaches(y) || !scope.reaches(out))
+    return fail(BX_EINVAL, "y or out lives on a GPU the compute device (x's / the stream's) cannot reach");
   const int64_t B = (int64_t)q * n;
   if (nblocks > (INT64_MAX - x_bit0) / B || nblocks > (INT64_MAX - y_bit0) / B)
     return fail(BX_EINVAL, "block range overflows");
@@ -202,7 +237,8 @@ int bx_pack(const void* samples, int elem_bytes, int b, int64_t count, void* out
   if (count == 0) return BX_OK;
   if (!samples || !out) return fail(BX_EINVAL, "null buffer");
   if ((uintptr_t)out & 3) return fail(BX_EINVAL, "out must be 4-byte aligned");
-  const DeviceScope scope(out);
+  const DeviceScope scope(samples, stream);
+  if (!scope.reaches(out)) return fail(BX_EINVAL, "out lives on a GPU the samples' device cannot reach");
   cudaError_t e = bx::launch_pack(samples, elem_bytes, b, count, out, out_bit0,
                                   static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_pack: ") + cudaGetErrorString(e));
@@ -215,7 +251,7 @@ int bx_bernoulli_bits(void* out, int64_t nbits, double p, uint64_t seed, int64_t
   if (nbits < 0 || bit0 < 0 || !(p >= 0.0 && p <= 1.0)) return fail(BX_EINVAL, "bad Bernoulli request");
   if (nbits == 0) return BX_OK;
   if (!out || ((uintptr_t)out & 3)) return fail(BX_EINVAL, "out must be a 4-byte aligned buffer");
-  const DeviceScope scope(out);
+  const DeviceScope scope(out, stream);
   cudaError_t e = bx::launch_bernoulli(static_cast<uint32_t*>(out), nbits, seed, bit0, p,
                                        static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_bernoulli_bits: ") + cudaGetErrorString(e));
@@ -233,7 +269,7 @@ int bx_xor_scan_rows(void* matrix, int64_t rows, int row_words, void* scratch, v
   if (rows <= 1) return BX_OK;
   if (!matrix || !scratch || ((uintptr_t)matrix & 3) || ((uintptr_t)scratch & 3))
     return fail(BX_EINVAL, "matrix and scratch must be 4-byte aligned device buffers");
-  const DeviceScope scope(matrix);
+  const DeviceScope scope(matrix, stream);
   cudaError_t e = bx::launch_xor_scan(static_cast<uint32_t*>(matrix), rows, row_words,
                                       static_cast<uint32_t*>(scratch), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_xor_scan_rows: ") + cudaGetErrorString(e));
@@ -252,7 +288,9 @@ int bx_markov_chain(const void* u, int64_t count, const void* cum, int b, int st
   if (start_state < 0 || start_state >= (1 << b)) return fail(BX_EINVAL, "start state out of range");
   if (count == 0) return BX_OK;
   if (!u || !cum || !values || !scratch) return fail(BX_EINVAL, "null buffer");
-  const DeviceScope scope(values);
+  const DeviceScope scope(u, stream);
+  if (!scope.reaches(values) || !scope.reaches(cum) || !scope.reaches(scratch))
+    return fail(BX_EINVAL, "markov buffers live on a GPU the compute device cannot reach");
   cudaError_t e = bx::launch_markov(static_cast<const double*>(u), count, static_cast<const double*>(cum),
                                     b, start_state, static_cast<uint16_t*>(values),
                                     static_cast<int*>(scratch), static_cast<cudaStream_t>(stream));
@@ -274,7 +312,7 @@ int bx_ip_table(int q, int n, uint32_t x0, uint32_t nx, void* out, void* stream)
   if (nx == 0) return BX_OK;
   if ((uint64_t)x0 + nx > (1ull << (q * n))) return fail(BX_EINVAL, "x range beyond 2^(q*n)");
   if (!out || ((uintptr_t)out & 1)) return fail(BX_EINVAL, "out must be a 2-byte aligned buffer");
-  const DeviceScope scope(out);
+  const DeviceScope scope(out, stream);
   cudaError_t e = bx::launch_ip_table(q, modulus_low(q), n, x0, nx, static_cast<uint16_t*>(out),
                                       static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_ip_table: ") + cudaGetErrorString(e));
@@ -287,7 +325,7 @@ int bx_ip_histograms(int q, int n, uint32_t d0, uint32_t nd, void* counts, void*
   if (nd == 0) return BX_OK;
   if ((uint64_t)d0 + nd > (1ull << (q * n))) return fail(BX_EINVAL, "d range beyond 2^(q*n)");
   if (!counts || ((uintptr_t)counts & 3)) return fail(BX_EINVAL, "counts must be 4-byte aligned");
-  const DeviceScope scope(counts);
+  const DeviceScope scope(counts, stream);
   cudaError_t e = bx::launch_ip_hist(q, modulus_low(q), n, d0, nd, static_cast<uint32_t*>(counts),
                                      static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_ip_histograms: ") + cudaGetErrorString(e));
@@ -299,7 +337,8 @@ int bx_rows_uniform(const void* counts, uint32_t nrows, uint32_t bins, uint32_t 
                     void* flags, void* stream) {
   if (nrows == 0) return BX_OK;
   if (!counts || !flags) return fail(BX_EINVAL, "null buffer");
-  const DeviceScope scope(counts);
+  const DeviceScope scope(counts, stream);
+  if (!scope.reaches(flags)) return fail(BX_EINVAL, "flags live on a GPU the counts' device cannot reach");
   cudaError_t e = bx::launch_rows_uniform(static_cast<const uint32_t*>(counts), nrows, bins, expected,
                                           static_cast<uint8_t*>(flags), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_rows_uniform: ") + cudaGetErrorString(e));
@@ -313,7 +352,9 @@ int bx_gf_ip_generic(int q, const void* modulus_low, const void* x, const void* 
   if (n < 1 || nvec < 0) return fail(BX_EINVAL, "n must be >= 1 and nvec >= 0");
   if (nvec == 0) return BX_OK;
   if (!modulus_low || !x || !y || !out) return fail(BX_EINVAL, "null buffer");
-  const DeviceScope scope(out);
+  const DeviceScope scope(x, stream);
+  if (!scope.reaches(y) || !scope.reaches(out) || !scope.reaches(modulus_low))
+    return fail(BX_EINVAL, "y, modulus or out lives on a GPU x's device cannot reach");
   cudaError_t e = bx::launch_gf_ip_generic(q, static_cast<const uint32_t*>(modulus_low),
                                            static_cast<const uint32_t*>(x), static_cast<const uint32_t*>(y),
                                            n, nvec, static_cast<uint32_t*>(out),

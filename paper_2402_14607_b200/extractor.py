@@ -36,6 +36,7 @@ from .report import ExtractionReport
 READ_CHUNK = 1 << 16          # BitReader chunk size (reference bitio.py:25)
 DEFAULT_SEGMENT_BLOCKS = 1 << 24
 FIRST_LAZY_SEGMENT = 4096        # first chunks of an iteration arrive after 4096 blocks
+ITER_PIECE = 1 << 16             # blocks unpacked at a time by __iter__ (multiple of 8)
 
 
 @dataclass(frozen=True)
@@ -82,14 +83,41 @@ class BlockProcessingError(RuntimeError):
 # ------------------------------------------------------------ device helpers
 
 def _pack_vectors(vectors: Sequence[Sequence[int]], q: int) -> bytes:
-    """Concatenate element vectors LSB-first into one q*n*len bit stream."""
-    acc = 0
-    pos = 0
-    for vec in vectors:
-        for v in vec:
-            acc |= v << pos
-            pos += q
-    return acc.to_bytes((pos + 7) // 8, "little")
+    """Concatenate element vectors LSB-first into one q*n*len bit stream.
+
+    Linear time: every element becomes ceil(q/8) little-endian bytes at a fixed
+    stride, the (elements x q) bit matrix is cut out of them and re-packed in
+    one ``packbits`` (no growing big-int shifts)."""
+    flat = [v for vec in vectors for v in vec]
+    if not flat:
+        return b""
+    nb = (q + 7) // 8
+    if q % 8 == 0 and q <= 64:
+        arr = np.array(flat, dtype=np.uint64).view(np.uint8).reshape(-1, 8)[:, :nb]
+        return arr.tobytes()
+    raw = np.frombuffer(b"".join(int(v).to_bytes(nb, "little") for v in flat),
+                        dtype=np.uint8).reshape(-1, nb)
+    bits = np.unpackbits(raw, axis=1, bitorder="little")[:, :q]
+    return np.packbits(bits.reshape(-1), bitorder="little").tobytes()
+
+
+def _unpack_fields(buf, count: int, q: int) -> list[int]:
+    """The `count` consecutive q-bit fields at the start of the LSB-first bit
+    string `buf`, as Python ints (linear time; inverse of ``_pack_vectors``)."""
+    if count <= 0:
+        return []
+    a = np.frombuffer(buf, dtype=np.uint8, count=(count * q + 7) // 8)
+    if q in (8, 16, 32, 64):
+        return a.view(f"<u{q // 8}").tolist()
+    bits = np.unpackbits(a, bitorder="little")[:count * q].reshape(count, q)
+    width = 64 if q <= 64 else 128
+    padded = np.zeros((count, width), dtype=np.uint8)
+    padded[:, :q] = bits
+    words = np.packbits(padded, axis=1, bitorder="little").view("<u8")
+    if q <= 64:
+        return words.reshape(-1).tolist()
+    lo, hi = words[:, 0].tolist(), words[:, 1].tolist()
+    return [a_ | (b_ << 64) for a_, b_ in zip(lo, hi)]
 
 
 def _generic_inner_products(q: int, modulus: int, xs, ys, dev) -> list[int]:
@@ -147,10 +175,8 @@ def _device_inner_products(q: int, xs: Sequence[Sequence[int]], ys: Sequence[Seq
         res = D.extract_eq(xd, xn, yd, yn, q, n, len(idx))
         nbytes = (len(idx) * q + 7) // 8
         host = res[:nbytes].cpu().numpy().tobytes()
-        val = int.from_bytes(host, "little")
-        mask = (1 << q) - 1
-        for k, i in enumerate(idx):
-            out[i] = (val >> (k * q)) & mask
+        for i, v in zip(idx, _unpack_fields(host, len(idx), q)):
+            out[i] = v
     return out
 
 
@@ -171,8 +197,11 @@ def run_parallel(blocks: Iterable[BlockPair], workers: int, *,
                  capacity: int | None = None) -> Iterator[OutputChunk]:
     """Inner products of BlockPairs, in block order (reference extractor.py:94-130).
 
-    Pairs are gathered into batches (``capacity`` pairs, default 4096) and each
-    batch is one device launch per (q, n) group.  Output is identical for every
+    Pairs are gathered into batches that grow 1, 2, 4, ... up to ``capacity``
+    pairs (default 4096); each batch is one device launch per (q, n) group.  If
+    the block source itself raises, the pairs already gathered are computed and
+    yielded first (as the reference's lazy workers=1 loop would have), then the
+    error propagates.  Output is identical for every
     ``workers`` value.  A pair with an out-of-range element raises ValueError at
     its position (workers == 1) or BlockProcessingError carrying its index
     (workers > 1), after all earlier chunks were yielded -- as the reference.
@@ -182,13 +211,21 @@ def run_parallel(blocks: Iterable[BlockPair], workers: int, *,
     batch_cap = capacity if capacity is not None else 4096
     batch_cap = max(1, batch_cap)
     it = iter(blocks)
-    while True:
+    size = 1                 # batches grow 1, 2, 4, ... up to batch_cap, so a live
+    while True:              # block source sees its first chunk after one pair
         batch: list[BlockPair] = []
-        for pair in it:
-            batch.append(pair)
-            if len(batch) >= batch_cap:
-                break
+        source_exc: BaseException | None = None
+        try:
+            for pair in it:
+                batch.append(pair)
+                if len(batch) >= size:
+                    break
+        except Exception as exc:  # noqa: BLE001 - the block source failed: flush, then re-raise
+            source_exc = exc
+        size = min(batch_cap, 2 * size)
         if not batch:
+            if source_exc is not None:
+                raise source_exc
             return
         bad_at = None
         bad_exc: Exception | None = None
@@ -221,6 +258,8 @@ def run_parallel(blocks: Iterable[BlockPair], workers: int, *,
             if workers == 1:
                 raise bad_exc
             raise BlockProcessingError(batch[bad_at].index, bad_exc) from bad_exc
+        if source_exc is not None:
+            raise source_exc
 
 
 # ---------------------------------------------------------- stream sources
@@ -679,11 +718,26 @@ class Extraction:
             for first, count, packed in self._segments():
                 widths = ([self.plan.field_bits] * count if self.mode == "eq"
                           else self._widths[first:first + count])
-                val = int.from_bytes(bytes(packed), "little")
-                pos = 0
+                buf = np.frombuffer(memoryview(packed), dtype=np.uint8) \
+                    if not isinstance(packed, np.ndarray) else packed.reshape(-1).view(np.uint8)
+                if widths and widths[0] == widths[-1] and len(set(widths)) == 1:
+                    # constant width: unpack ITER_PIECE blocks at a time (pieces
+                    # start on byte boundaries), linear in the segment length
+                    w = widths[0]
+                    for p0 in range(0, count, ITER_PIECE):
+                        c = min(ITER_PIECE, count - p0)
+                        lo = p0 * w // 8
+                        vals = _unpack_fields(buf[lo:lo + (c * w + 7) // 8], c, w)
+                        for k, bits in enumerate(vals):
+                            self._chunks_emitted += 1
+                            self._output_bits += w
+                            yield OutputChunk(first + p0 + k + 1, bits, w)
+                    continue
+                # growing widths (neq, <= 128 blocks before the width cap)
+                val = int.from_bytes(buf.tobytes(), "little")
                 for k, w in enumerate(widths):
-                    bits = (val >> pos) & ((1 << w) - 1)
-                    pos += w
+                    bits = val & ((1 << w) - 1)
+                    val >>= w
                     self._chunks_emitted += 1
                     self._output_bits += w
                     yield OutputChunk(first + k + 1, bits, w)

@@ -336,7 +336,8 @@ def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit
 
 def distributed_extract(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0,
                         y_bit0: int = 0, group=None, compute=None, device=None,
-                        gather: str = "object", to_host: bool = True):
+                        gather: str = "object", to_host: bool = True,
+                        local_input: bool = False):
     """Multi-process form (one process per GPU, torch.distributed).
 
     Every rank sees the same run (e.g. a shared capture file or a shared seeded
@@ -370,7 +371,7 @@ def distributed_extract(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0,
     B = q * n
     part = b""
     if cnt:
-        xs, ys = x_bit0 + start * B, y_bit0 + start * B
+        xs, ys = (x_bit0, y_bit0) if local_input else (x_bit0 + start * B, y_bit0 + start * B)
         fn = compute or (lambda *a, **k: extract_packed(*a, device=device, **k))
         part = fn(xv[xs // 8:(xs + cnt * B + 7) // 8], yv[ys // 8:(ys + cnt * B + 7) // 8],
                   q, n, cnt, x_bit0=xs % 8, y_bit0=ys % 8)
@@ -387,7 +388,7 @@ def distributed_extract(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0,
 
 
 def _distributed_extract_peer(xv, yv, q: int, n: int, count: int, *, x_bit0: int, y_bit0: int,
-                              group, device, to_host: bool):
+                              group, device, to_host: bool, local_input: bool = False):
     """gather="peer" of :func:`distributed_extract`."""
     import torch
     import torch.distributed as dist
@@ -412,7 +413,7 @@ def _distributed_extract_peer(xv, yv, q: int, n: int, count: int, *, x_bit0: int
     start, cnt = rank_range(count, rank, world)
     B = q * n
     if cnt:
-        xs, ys = x_bit0 + start * B, y_bit0 + start * B
+        xs, ys = (x_bit0, y_bit0) if local_input else (x_bit0 + start * B, y_bit0 + start * B)
         _extract_one_device(_slice(xv, xs // 8, (xs + cnt * B + 7) // 8),
                             _slice(yv, ys // 8, (ys + cnt * B + 7) // 8),
                             q, n, cnt, xs % 8, ys % 8, dev, None, 0,

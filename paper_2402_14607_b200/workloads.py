@@ -20,6 +20,7 @@ Nothing here touches the GPU; the device-side generators live in ``sources``.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -273,6 +274,83 @@ def to_model(spec: SourceSpec):
     if spec.kind == "iid-table":
         return S.iid_table(spec.pmf(), spec.bits_per_sample, seed=spec.seed)
     raise ValueError(f"no reference model for {spec.kind}")
+
+
+def _draw_into(spec: SourceSpec, start: int, out: np.ndarray) -> None:
+    """PCG64 doubles for samples [start, start+len(out)) of an iid stream,
+    written in place (one 64-bit step per sample, reference sources.py:133-140)."""
+    rng = np.random.default_rng(spec.seed)
+    if start:
+        rng.bit_generator.advance(start)
+    rng.random(out.size, out=out)
+
+
+def stream_range_device(spec: SourceSpec, start: int, count: int, device=None, *,
+                        chunk: int = 1 << 22, threads: int | None = None):
+    """Samples [start, start+count) of an iid stream as a packed, padded device
+    buffer: ``(buffer, nbytes)``, byte-identical to the same slice of the
+    reference ``generate`` output (sources.py:124-140).
+
+    The PCG64 draws are the only host work; they are split into chunks drawn
+    by ``threads`` host threads at once (each chunk from its own generator
+    advanced to the chunk's first sample, numpy releases the GIL), straight
+    into pinned buffers, while the device maps the previous wave of chunks to
+    samples (threshold / inverse-CDF search, as numpy's ``choice`` does) and
+    packs them (``bx_pack``).  This is how a rank of a sharded run generates
+    only its own block range (sharding.shard_ranges).
+    """
+    import concurrent.futures as cf
+
+    import torch
+
+    from . import device as D
+
+    if spec.kind not in ("iid-biased", "iid-table"):
+        raise ValueError(f"range generation needs an iid kind, not {spec.kind}")
+    b = spec.bits_per_sample
+    if count < 1:
+        raise ValueError("count must be >= 1")
+    if (start * b) % 8:
+        raise ValueError("range must start on a byte boundary of the stream")
+    dev = D.require_cuda(device)
+    nbytes = (count * b + 7) // 8
+    out = D.empty_stream(nbytes, dev)
+    out[(count * b // 32) * 4:].zero_()
+    threads = threads or max(1, min(16, os.cpu_count() or 1))
+    chunk = max(64, chunk // 64 * 64)         # whole words of output for b >= 1
+    spans = [(s, min(chunk, count - s)) for s in range(0, count, chunk)]
+    banks = [[torch.empty(chunk, dtype=torch.float64, pin_memory=True) for _ in range(threads)]
+             for _ in range(2)]
+    done = [None, None]
+    stream = torch.cuda.Stream(dev)
+    cdf_d = None
+    if spec.kind == "iid-table":
+        cdf = np.cumsum(spec.pmf())
+        cdf /= cdf[-1]
+        cdf_d = torch.from_numpy(cdf).to(dev)
+    with cf.ThreadPoolExecutor(threads, thread_name_prefix="bx-draw") as pool, \
+            torch.cuda.device(dev):
+        for w in range(0, len(spans), threads):
+            bank = banks[(w // threads) % 2]
+            if done[(w // threads) % 2] is not None:
+                done[(w // threads) % 2].synchronize()     # bank's previous H2D finished
+            wave = spans[w:w + threads]
+            list(pool.map(lambda a: _draw_into(spec, start + a[1][0], bank[a[0]][:a[1][1]].numpy()),
+                          enumerate(wave)))
+            with torch.cuda.stream(stream):
+                for i, (s, c) in enumerate(wave):
+                    u = bank[i][:c].to(dev, non_blocking=True)
+                    if spec.kind == "iid-biased":
+                        vals = (u < spec.p).to(torch.uint8)
+                    else:
+                        vals = torch.searchsorted(cdf_d, u, right=True).to(torch.uint8)
+                    D.pack(vals, b, out=out, out_bit0=s * b, stream=stream)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+            done[(w // threads) % 2] = ev
+        stream.synchronize()
+    out.record_stream(stream)
+    return out, nbytes
 
 
 def stream_device(spec: SourceSpec, samples: int, device=None):

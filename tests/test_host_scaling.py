@@ -1,0 +1,155 @@
+"""Host-side paths of the drop-in API run in linear time (CPU, device stubbed).
+
+The packed device output is unpacked into OutputChunks, and BlockPair element
+vectors are packed into device streams, without growing big-int shifts:
+doubling the work must not much more than double the time, and the sizes the
+reference handles in seconds finish well under a second here.
+"""
+import time
+
+import numpy as np
+import pytest
+
+from paper_2402_14607_b200 import extractor as E
+from paper_2402_14607_b200 import sharding
+
+
+def _bigint_pack(vectors, q):
+    acc, pos = 0, 0
+    for vec in vectors:
+        for v in vec:
+            acc |= v << pos
+            pos += q
+    return acc.to_bytes((pos + 7) // 8, "little")
+
+
+@pytest.mark.parametrize("q", [1, 2, 3, 4, 7, 8, 13, 16, 32, 56, 63, 64, 65, 80, 127, 128])
+def test_pack_unpack_round_trip(q):
+    rng = np.random.default_rng(q)
+    vecs = [[int.from_bytes(rng.bytes(16), "little") & ((1 << q) - 1) for _ in range(int(rng.integers(1, 9)))]
+            for _ in range(37)]
+    packed = E._pack_vectors(vecs, q)
+    assert packed == _bigint_pack(vecs, q)
+    flat = [v for vec in vecs for v in vec]
+    assert E._unpack_fields(packed, len(flat), q) == flat
+
+
+def test_pack_paper_batch_is_fast():
+    """One default 4096-pair run_parallel batch at the paper shape (q=80, n=71):
+    144 s per operand with the old big-int accumulator."""
+    rng = np.random.default_rng(0)
+    q, n = 80, 71
+    vecs = [[int.from_bytes(rng.bytes(10), "little") for _ in range(n)] for _ in range(4096)]
+    t0 = time.perf_counter()
+    packed = E._pack_vectors(vecs, q)
+    vals = E._unpack_fields(packed, 4096 * n, q)
+    dt = time.perf_counter() - t0
+    assert vals[:5] == vecs[0][:5] and vals[-1] == vecs[-1][-1]
+    assert dt < 2.0, dt
+
+
+def _stub_device(monkeypatch):
+    def fake(xv, yv, q, n, count, *, x_bit0=0, y_bit0=0, device=None, devices=None, out=None):
+        nbytes = (count * q + 7) // 8
+        if out is not None:
+            return out[:nbytes].numpy()
+        return np.full(nbytes, 0xA5, dtype=np.uint8)
+    monkeypatch.setattr(sharding, "extract_packed", fake)
+
+
+def _iterate(nblocks, q=4, n=64):
+    from fractions import Fraction
+
+    import paper_2402_14607_b200 as bx
+
+    nbytes = nblocks * q * n // 8
+    data = bytes(nbytes)
+    plan = bx.EqPlan(8, nbytes, Fraction(3, 4), Fraction(1, 2), n, q, nblocks, nblocks * q, 0.0)
+    t0 = time.perf_counter()
+    k = 0
+    last = None
+    for ch in bx.extract_eq(data, data, plan):
+        k += 1
+        last = ch
+    dt = time.perf_counter() - t0
+    assert k == nblocks and last.index == nblocks and last.width == q
+    return dt
+
+
+def test_iteration_is_linear(monkeypatch):
+    """Extraction.__iter__ over 2^19 vs 2^21 blocks (q=4, n=64, c2's shape):
+    the per-chunk cost stays flat (it doubled with every doubling before)."""
+    _stub_device(monkeypatch)
+    _iterate(1 << 12)
+    t1 = _iterate(1 << 19)
+    t4 = _iterate(1 << 21)
+    assert t4 / t1 < 6.0, (t1, t4)
+    # c2 (8,388,608 blocks) extrapolates to ~4*t4; the reference needs ~12 min
+    assert t4 < 30.0, t4
+
+
+def test_iteration_values_from_packed(monkeypatch):
+    """Chunks carry the right bits when the packed output is unpacked piecewise."""
+    from fractions import Fraction
+
+    import paper_2402_14607_b200 as bx
+
+    q, n, nblocks = 12, 8, 3 * E.ITER_PIECE + 77
+    rng = np.random.default_rng(5)
+    packed = np.frombuffer(rng.bytes((nblocks * q + 7) // 8), dtype=np.uint8).copy()
+    packed[-1] &= (1 << ((nblocks * q) % 8 or 8)) - 1
+
+    def fake(xv, yv, q_, n_, count, *, x_bit0=0, y_bit0=0, device=None, devices=None, out=None):
+        lo = x_bit0  # segments start at block 0 in this test (one segment)
+        assert lo == 0 and count == nblocks
+        return packed
+    monkeypatch.setattr(sharding, "extract_packed", fake)
+    monkeypatch.setattr(E, "FIRST_LAZY_SEGMENT", 1 << 20)
+    nbytes = nblocks * q * n // 8
+    plan = bx.EqPlan(8, nbytes, Fraction(3, 4), Fraction(1, 2), n, q, nblocks, nblocks * q, 0.0)
+    got = [c.bits for c in bx.extract_eq(bytes(nbytes), bytes(nbytes), plan)]
+    val = int.from_bytes(packed.tobytes(), "little")
+    want = [(val >> (k * q)) & ((1 << q) - 1) for k in (0, 1, E.ITER_PIECE - 1, E.ITER_PIECE, nblocks - 1)]
+    assert [got[k] for k in (0, 1, E.ITER_PIECE - 1, E.ITER_PIECE, nblocks - 1)] == want
+    assert len(got) == nblocks
+
+
+def test_run_parallel_flushes_before_source_error(monkeypatch):
+    """A failing block source: every pair gathered before the failure is
+    computed and yielded, then the source's exception propagates."""
+    import paper_2402_14607_b200 as bx
+
+    monkeypatch.setattr(E, "_device_inner_products",
+                        lambda q, xs, ys, device=None, modulus=None: [len(x) for x in xs])
+    ctx = bx.field(8)
+
+    def blocks():
+        for i in range(1, 11):
+            yield E.BlockPair(i, ctx, (1,) * i, (1,) * i)
+        raise OSError("source died")
+
+    got = []
+    with pytest.raises(OSError, match="source died"):
+        for ch in E.run_parallel(blocks(), workers=1):
+            got.append(ch.index)
+    assert got == list(range(1, 11))
+
+
+def test_run_parallel_first_chunk_after_one_pair(monkeypatch):
+    """Batches start at one pair, so a live source sees its first chunk before
+    it must produce a second pair (the reference's workers=1 laziness)."""
+    import paper_2402_14607_b200 as bx
+
+    monkeypatch.setattr(E, "_device_inner_products",
+                        lambda q, xs, ys, device=None, modulus=None: [0 for _ in xs])
+    ctx = bx.field(4)
+    pulled = []
+
+    def blocks():
+        for i in range(1, 100):
+            pulled.append(i)
+            yield E.BlockPair(i, ctx, (1, 2), (3, 4))
+
+    it = E.run_parallel(blocks(), workers=1)
+    first = next(it)
+    assert first.index == 1 and pulled == [1]
