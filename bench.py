@@ -60,6 +60,11 @@ LOP3_PER_S = 18.40e12
 LOP3_SOURCE = "measured LOP3 rate 18.40 T/s x 32 pairs (profiles/r01_pipes_microbench.txt)"
 UNIT = "Gbit/s raw input (both sources, whole job)"
 SWEEPS = {"c5": ["c5_n128", "c5_n256", "c5_n512", "c5_n1024", "c5_n2048"]}
+# raw-sample packer workloads (reference sources.py:116-121):
+# name -> (sample bytes, bits per sample); 2^28 samples each (config 2's size)
+PACK_WORKLOADS = {"pack_b1": (1, 1), "pack_b6": (1, 6), "pack_b12": (2, 12), "pack_b14": (2, 14)}
+PACK_SAMPLES = 1 << 28
+PACK_REF_MAX = 1 << 24   # reference numpy packer temporaries are 8*b bytes per sample
 REF_DIR = REPO / "baseline" / "_ref"
 
 
@@ -646,6 +651,156 @@ def run_ours(args, wls) -> None:
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------ packer workloads
+
+def _pack_samples_host(elem: int, b: int, count: int, seed: int = 11):
+    import numpy as np
+
+    dt = np.dtype(f"u{elem}")
+    return np.random.default_rng(seed).integers(0, (1 << b) - 1, size=count, dtype=dt,
+                                                endpoint=True)
+
+
+def _pack_reference_rate(elem: int, b: int, target_s: float) -> dict:
+    """The reference's own _pack_samples (numpy, one core) from baseline/_ref on
+    a bounded sample, checked against bx_pack's output for the same values;
+    the C oracle (bxo_pack) when baseline/_ref is absent."""
+    import numpy as np
+
+    ref = _reference_module()
+    k = 1 << 16
+    while True:
+        vals = _pack_samples_host(elem, b, k, seed=12)
+        t0 = time.perf_counter()
+        if ref is not None:
+            from blockext import sources as ref_sources
+            got = ref_sources._pack_samples(vals.astype(np.uint64), b)
+        else:
+            from oracle import coracle
+            got = coracle.pack(vals.tolist(), b)
+        dt = time.perf_counter() - t0
+        if dt >= target_s / 2 or k >= PACK_REF_MAX:
+            break
+        k = min(PACK_REF_MAX, k * 4)
+    return {"samples": k, "seconds": dt, "gsamples_s": k / dt / 1e9,
+            "gbs": k * (elem + b / 8) / dt / 1e9, "vals": vals, "out": got,
+            "kind": "reference" if ref is not None else "port",
+            "impl": ("baseline/_ref blockext.sources._pack_samples (numpy)" if ref is not None
+                     else "oracle/bx_oracle.c bxo_pack")}
+
+
+def run_pack(args) -> None:
+    """--workload pack_bN: bx_pack over 2^28 resident samples per step."""
+    import numpy as np
+    import torch
+
+    from paper_2402_14607_b200 import _lib, device as D
+
+    world, rank, local = _dist()
+    if rank != 0:
+        return
+    elem, b = PACK_WORKLOADS[args.workload]
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    count = PACK_SAMPLES
+    host = _pack_samples_host(elem, b, count)
+    hs = torch.from_numpy(host.view(np.dtype(f"i{elem}")) if elem > 1 else host).pin_memory()
+    sd = hs.to(dev)
+    nbytes = (count * b + 7) // 8
+    out = D.empty_stream(nbytes, dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        D.pack(sd, b, out=out, stream=stream)
+    torch.cuda.synchronize(dev)
+    # parity of the resident run: the whole output against a numpy unpack
+    bits = np.unpackbits(out[:nbytes].cpu().numpy(), bitorder="little")
+    back = bits.reshape(-1, b).astype(np.uint64) @ (np.uint64(1) << np.arange(b, dtype=np.uint64))
+    parity_ok = bool(np.array_equal(back, host.astype(np.uint64)))
+    del bits, back
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    sampler = ClockSampler(local)
+    n0 = _lib.launch_count()
+    with sampler:
+        torch.cuda.synchronize(dev)
+        evs[0].record(stream)
+        for i in range(args.steps):
+            D.pack(sd, b, out=out, stream=stream)    # 2^28 samples > L2: no flush
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = _lib.launch_count() - n0
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    ms = sum(per) / args.steps
+    alg_bytes = count * elem + nbytes
+    peak, peak_src = _peaks()
+    achieved = alg_bytes / (ms * 1e-3) / 1e9
+    # e2e: pinned host samples -> H2D -> bx_pack -> D2H of the packed stream
+    oh = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    e2e_steps = max(1, min(args.steps, 5))
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        s_dev = hs.to(dev, non_blocking=True)
+        o = D.pack(s_dev, b)
+        oh.copy_(o[:nbytes], non_blocking=True)
+        torch.cuda.synchronize(dev)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_ok = bytes(oh.numpy()[:1 << 20]) == bytes(out[:1 << 20].cpu().numpy())
+    cpu = None
+    if not args.no_cpu:
+        r = _pack_reference_rate(elem, b, args.cpu_seconds)
+        sd_small = torch.from_numpy(r["vals"].view(np.dtype(f"i{elem}")) if elem > 1
+                                    else r["vals"]).to(dev)
+        mine = D.pack(sd_small, b)[:len(r["out"])].cpu().numpy().tobytes()
+        cpu = {"value": r["gsamples_s"], "unit": "Gsamples/s", "cores": 1, "kind": r["kind"],
+               "sample": f"{r['samples']} samples of the same distribution, {r['impl']}",
+               "gbs": r["gbs"], "matches_gpu_output": mine == r["out"]}
+    line = {
+        "metric": METRIC + " -- raw-sample packer (bx_pack) leg",
+        "value": count / (ms * 1e-3) / 1e9, "unit": "Gsamples/s packed",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": f"u{8 * elem}", "data": "synthetic (seeded uniform b-bit samples)",
+        "config": {"workload": args.workload, "samples": count, "sample_bytes": elem,
+                   "bits_per_sample": b, "packed_bytes": nbytes,
+                   "l2": "inputs exceed the L2 (no flush needed)",
+                   "reference": "sources._pack_samples, pkg/src/blockext/sources.py:116-121"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _traffic(args.workload),
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel_ms": ms, "kernel": f"bx::pack_tile_kernel<uint{8 * elem}, {b}>"},
+        "e2e": {"value": count / e2e_s / 1e9, "unit": "Gsamples/s packed",
+                "h2d_bytes_per_step": count * elem, "d2h_bytes_per_step": nbytes,
+                "seconds_per_step": e2e_s, "steps": e2e_steps, "bit_exact_vs_device_run": e2e_ok,
+                "path": "pinned host samples -> device.pack (bx_pack) -> pinned host bytes"},
+        "cpu_baseline": cpu, "clocks": sampler.summary(), "gpu_launches": launches,
+        "parity": {"whole_output_vs_numpy_unpack": parity_ok},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_pack_reference(args) -> None:
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    elem, b = PACK_WORKLOADS[args.workload]
+    for _ in range(args.warmup):
+        _pack_reference_rate(elem, b, 1.0)
+    rates = [_pack_reference_rate(elem, b, 4.0) for _ in range(args.steps)]
+    g = sum(r["samples"] for r in rates) / sum(r["seconds"] for r in rates) / 1e9
+    r = rates[-1]
+    line = {"impl": "reference", "metric": METRIC + " -- raw-sample packer (bx_pack) leg",
+            "value": g, "unit": "Gsamples/s packed", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["seconds"] * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": f"u{8 * elem}",
+            "data": "synthetic (seeded uniform b-bit samples)",
+            "config": {"workload": args.workload, "samples_per_step": r["samples"]},
+            "cpu_baseline": {"value": g, "unit": "Gsamples/s", "cores": 1, "kind": r["kind"],
+                             "sample": f"{r['samples']} samples per step, {r['impl']}"},
+            "e2e": {"value": g, "unit": "Gsamples/s packed", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
 class _Null:
     def __enter__(self):
         return self
@@ -733,6 +888,9 @@ def main(argv=None) -> int:
         args.warmup = 3            # contract: W >= 3
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         return _relaunch(args.gpus, argv)
+    if args.workload in PACK_WORKLOADS:
+        (run_pack_reference if args.impl == "reference" else run_pack)(args)
+        return 0
     wls = _workloads(args.workload)
     if args.impl == "reference":
         run_reference(args, wls)

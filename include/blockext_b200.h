@@ -110,23 +110,50 @@ int bx_pack(const void* samples, int elem_bytes, int b, int64_t count,
 int bx_gf_ip_generic(int q, const void* modulus_low, const void* x, const void* y, int n,
                      int64_t nvec, void* out, void* stream);
 
+/*
+ * Powers over GF(2^q) with a caller-chosen modulus (GFContext.pow / inv,
+ * reference gf2q.py:171-189): out[v] = x[v]^e[v], square-and-multiply over
+ * e's bits in one launch (one thread per element).  x, e, out: count 128-bit
+ * little-endian values; modulus_low as for bx_gf_ip_generic.  Callers reduce
+ * e modulo 2^q - 1 for nonzero x (the multiplicative group's order).
+ */
+int bx_gf_pow(int q, const void* modulus_low, const void* x, const void* e, int64_t count,
+              void* out, void* stream);
+
 /* ---- native streaming pipeline ----------------- */
 
 /*
  * Push-based equal-width extraction for producers outside Python.  Each push
  * hands over the next nbytes (<= chunk_bytes) of both streams from host
- * memory; every block completed by the bytes so far is extracted on `device`
- * and the packed output's whole bytes are written to out (capacity out_cap),
- * *out_bytes = count.  Partial blocks and the last partial output byte carry
- * over, so the concatenated outputs of any push sequence (plus flush) equal
- * one run over the concatenated streams.  Synchronous per push.
+ * memory (copied before the call returns, so the caller may reuse them);
+ * every block completed by the bytes so far is extracted on `device`.
+ * Partial blocks and the last partial output byte carry over, so the
+ * concatenated outputs of any push sequence (then drain, then flush) equal
+ * one run over the concatenated streams (reference extractor.py:182-208,
+ * bitio.py:74-88; replaces the reference CLI's file loop, cli.py:88-129).
+ *
+ * bx_pipe_create: synchronous pipe -- each push returns its own output.
+ * bx_pipe_create_async: `depth` (1..4) pushes in flight; a push enqueues its
+ *   host copy, H2D, kernel and D2H and returns the output of the pushes
+ *   older than the newest depth-1 (depth 2: push k returns push k-1's bytes,
+ *   and push k's copies overlap push k-1's kernel and D2H).
+ * The whole output bytes returned by a call are written to out (capacity
+ * out_cap; bx_pipe_max_output(p) bytes per retired push suffice),
+ * *out_bytes = count.  Errors set bx_last_error(); after a BX_ECUDA the pipe
+ * must be destroyed.
  */
 typedef struct bx_pipe bx_pipe;
 bx_pipe* bx_pipe_create(int q, int n, int64_t chunk_bytes, int device);
+bx_pipe* bx_pipe_create_async(int q, int n, int64_t chunk_bytes, int device, int depth);
 int bx_pipe_push(bx_pipe* p, const void* x, const void* y, int64_t nbytes, void* out,
                  int64_t out_cap, int64_t* out_bytes);
-/* Emits the carried partial output byte (zero padded), if any. */
+/* Waits for every push in flight and writes their output (async pipes). */
+int bx_pipe_drain(bx_pipe* p, void* out, int64_t out_cap, int64_t* out_bytes);
+/* Emits the carried partial output byte (zero padded), if any; requires
+ * nothing in flight (drain first). */
 int bx_pipe_flush(bx_pipe* p, void* out, int64_t* out_bytes);
+/* Largest output one push (or one retired push in a drain) can produce. */
+int64_t bx_pipe_max_output(const bx_pipe* p);
 /* Blocks extracted so far (or -1 for NULL). */
 int64_t bx_pipe_blocks(const bx_pipe* p);
 void bx_pipe_destroy(bx_pipe* p);

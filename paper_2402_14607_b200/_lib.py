@@ -38,6 +38,10 @@ SIGNATURES = {
     "bx_pipe_create": (_vp, [_i32, _i32, _i64, _i32]),
     "bx_pipe_push": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _PI64]),
     "bx_pipe_flush": (_i32, [_vp, _vp, _PI64]),
+    "bx_pipe_create_async": (_vp, [_i32, _i32, _i64, _i32, _i32]),
+    "bx_gf_pow": (_i32, [_i32, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "bx_pipe_drain": (_i32, [_vp, _vp, _i64, _PI64]),
+    "bx_pipe_max_output": (_i64, [_vp]),
     "bx_pipe_blocks": (_i64, [_vp]),
     "bx_pipe_destroy": (None, [_vp]),
     "bx_bernoulli_bits": (_i32, [_vp, _i64, ctypes.c_double, ctypes.c_uint64, _i64, _vp]),

@@ -12,7 +12,7 @@
 #include "bx_launch.cuh"
 
 namespace bx {
-cudaError_t launch_pack(const void*, int, int, int64_t, void*, int64_t, cudaStream_t);
+cudaError_t launch_pack(const void*, int, int, int64_t, void*, int64_t, cudaStream_t, int*);
 cudaError_t launch_bernoulli(uint32_t*, int64_t, uint64_t, int64_t, double, cudaStream_t);
 int64_t xor_scan_scratch_words(int64_t, int);
 cudaError_t launch_xor_scan(uint32_t*, int64_t, int, uint32_t*, cudaStream_t);
@@ -23,6 +23,8 @@ cudaError_t launch_ip_table(int, uint32_t, int, uint32_t, uint32_t, uint16_t*, c
 cudaError_t launch_ip_hist(int, uint32_t, int, uint32_t, uint32_t, uint32_t*, cudaStream_t);
 cudaError_t launch_rows_uniform(const uint32_t*, uint32_t, uint32_t, uint32_t, uint8_t*,
                                 cudaStream_t);
+cudaError_t launch_gf_pow(int, const uint32_t*, const uint32_t*, const uint32_t*, int64_t, uint32_t*,
+                          cudaStream_t);
 cudaError_t launch_gf_ip_generic(int, const uint32_t*, const uint32_t*, const uint32_t*, int, int64_t,
                                  uint32_t*, cudaStream_t);
 
@@ -114,6 +116,14 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+}  // namespace
+
+namespace bx {
+// error reporting for the other translation units (bx_pipe.cu)
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace bx
+
+namespace {
 const std::array<bx::LaunchFn, 128>& table() {
   static const auto t = bx::make_table(std::make_integer_sequence<int, 128>{});
   return t;
@@ -239,10 +249,11 @@ int bx_pack(const void* samples, int elem_bytes, int b, int64_t count, void* out
   if ((uintptr_t)out & 3) return fail(BX_EINVAL, "out must be 4-byte aligned");
   const DeviceScope scope(samples, stream);
   if (!scope.reaches(out)) return fail(BX_EINVAL, "out lives on a GPU the samples' device cannot reach");
+  int launched = 0;
   cudaError_t e = bx::launch_pack(samples, elem_bytes, b, count, out, out_bit0,
-                                  static_cast<cudaStream_t>(stream));
+                                  static_cast<cudaStream_t>(stream), &launched);
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_pack: ") + cudaGetErrorString(e));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  g_launches.fetch_add(launched, std::memory_order_relaxed);
   return BX_OK;
 }
 
@@ -342,6 +353,24 @@ int bx_rows_uniform(const void* counts, uint32_t nrows, uint32_t bins, uint32_t 
   cudaError_t e = bx::launch_rows_uniform(static_cast<const uint32_t*>(counts), nrows, bins, expected,
                                           static_cast<uint8_t*>(flags), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_rows_uniform: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int bx_gf_pow(int q, const void* modulus_low, const void* x, const void* e, int64_t count, void* out,
+              void* stream) {
+  if (q < 1 || q > 128) return fail(BX_ERANGE, "field width outside 1..128");
+  if (count < 0) return fail(BX_EINVAL, "count must be >= 0");
+  if (count == 0) return BX_OK;
+  if (!modulus_low || !x || !e || !out) return fail(BX_EINVAL, "null buffer");
+  const DeviceScope scope(x, stream);
+  if (!scope.reaches(e) || !scope.reaches(out) || !scope.reaches(modulus_low))
+    return fail(BX_EINVAL, "e, modulus or out lives on a GPU x's device cannot reach");
+  cudaError_t err = bx::launch_gf_pow(q, static_cast<const uint32_t*>(modulus_low),
+                                      static_cast<const uint32_t*>(x), static_cast<const uint32_t*>(e),
+                                      count, static_cast<uint32_t*>(out),
+                                      static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return fail(BX_ECUDA, std::string("bx_gf_pow: ") + cudaGetErrorString(err));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return BX_OK;
 }

@@ -167,6 +167,65 @@ __global__ void gf_ip_generic_kernel(int q, const uint32_t* modulus, const uint3
   }
 }
 
+// c = a * b mod (x^q + m) for q-bit a, b (4-word operands)
+__device__ __forceinline__ void mulmod128(int q, const uint32_t (&m)[4], const uint32_t (&a)[4],
+                                          const uint32_t (&b)[4], uint32_t (&r)[4]) {
+  uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < q; i++)
+    if ((a[i >> 5] >> (i & 31)) & 1u) shl_xor8(c, b, i);
+  for (int i = 2 * q - 2; i >= q; i--) {
+    if ((c[i >> 5] >> (i & 31)) & 1u) {
+      c[i >> 5] ^= 1u << (i & 31);
+      shl_xor8(c, m, i - q);
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < 4; w++) {
+    const int lo = 32 * w;
+    uint32_t val = c[w];
+    if (lo >= q) val = 0;
+    else if (q - lo < 32) val &= (1u << (q - lo)) - 1u;
+    r[w] = val;
+  }
+}
+
+// out[v] = x[v]^e[v] by square-and-multiply over the exponent's bits, LSB
+// first (the reference GFContext.pow loop, gf2q.py:171-182), one thread per
+// element; 128-bit little-endian operands.
+__global__ void gf_pow_kernel(int q, const uint32_t* modulus, const uint32_t* x, const uint32_t* e,
+                              int64_t count, uint32_t* out) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= count) return;
+  const uint32_t m[4] = {modulus[0], modulus[1], modulus[2], modulus[3]};
+  uint32_t b[4] = {x[v * 4], x[v * 4 + 1], x[v * 4 + 2], x[v * 4 + 3]};
+  uint32_t r[4] = {1u, 0u, 0u, 0u};
+  int top = -1;
+  for (int i = 127; i >= 0 && top < 0; i--)
+    if ((e[v * 4 + (i >> 5)] >> (i & 31)) & 1u) top = i;
+  for (int i = 0; i <= top; i++) {
+    uint32_t t[4];
+    if ((e[v * 4 + (i >> 5)] >> (i & 31)) & 1u) {
+      mulmod128(q, m, r, b, t);
+#pragma unroll
+      for (int w = 0; w < 4; w++) r[w] = t[w];
+    }
+    if (i < top) {
+      mulmod128(q, m, b, b, t);
+#pragma unroll
+      for (int w = 0; w < 4; w++) b[w] = t[w];
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < 4; w++) out[v * 4 + w] = r[w];
+}
+
+cudaError_t launch_gf_pow(int q, const uint32_t* modulus, const uint32_t* x, const uint32_t* e,
+                          int64_t count, uint32_t* out, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  gf_pow_kernel<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(q, modulus, x, e, count, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gf_ip_generic(int q, const uint32_t* modulus, const uint32_t* x, const uint32_t* y,
                                  int n, int64_t nvec, uint32_t* out, cudaStream_t st) {
   if (nvec <= 0) return cudaSuccess;

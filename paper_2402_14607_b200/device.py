@@ -86,6 +86,15 @@ def pack(samples: torch.Tensor, b: int, *, out: torch.Tensor | None = None, out_
     elem = samples.element_size()
     if elem not in (1, 2, 4, 8) or samples.is_floating_point():
         raise ValueError("samples must be an integer tensor of 1, 2, 4 or 8 byte elements")
+    if not 1 <= b <= 8 * elem:
+        raise ValueError(f"bits per sample {b} outside 1..{8 * elem}")
+    nat = 1 if b <= 8 else 2 if b <= 16 else 4 if b <= 32 else 8
+    if elem > nat and not (elem == 2 and b <= 8) and samples.numel() >= 4096:
+        # keep the low `nat` bytes of every (little-endian) sample so the tile
+        # kernel for the natural type runs: an exact bit slice, not a cast
+        narrow = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[nat]
+        samples = samples.contiguous().view(narrow).view(-1, elem // nat)[:, 0].contiguous()
+        elem = nat
     count = samples.numel()
     if out is None:
         end = out_bit0 + count * b

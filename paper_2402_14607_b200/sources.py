@@ -158,9 +158,15 @@ def _pack_samples(values, bits_per_sample: int) -> bytes:
     from . import device as D
 
     dev = D.require_cuda()
-    arr = np.asarray(values).astype(np.uint64, copy=False).view(np.int64)
-    t = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
     b = bits_per_sample
+    arr = np.asarray(values).astype(np.uint64, copy=False)
+    if b < 64:
+        # the low b bits in the narrowest type that holds them (less H2D, and
+        # the packer's tile kernel for that type)
+        nat = np.uint8 if b <= 8 else np.uint16 if b <= 16 else np.uint32 if b <= 32 else np.uint64
+        arr = (arr & np.uint64((1 << b) - 1)).astype(nat)
+    t = torch.from_numpy(np.ascontiguousarray(arr).view(np.dtype(f"i{arr.itemsize}")) if arr.itemsize > 1
+                         else np.ascontiguousarray(arr)).to(dev)
     nbytes = (arr.size * b + 7) // 8
     return D.pack(t, b)[:nbytes].cpu().numpy().tobytes()
 

@@ -125,6 +125,49 @@ def test_field_inverses_small():
             assert len(set(row)) == (1 << q) - 1  # multiplication by x is a bijection
 
 
+def test_field_pow_and_inv_one_launch():
+    """GFContext.pow / inv (reference gf2q.py:171-189) as one bx_gf_pow launch,
+    against square-and-multiply over the oracle's field product; exponents
+    beyond 128 bits, e = 0, x = 0, the default and a custom modulus."""
+    from oracle import pyoracle
+    from paper_2402_14607_b200 import _lib
+    rnd = random.Random(77)
+
+    def ref_pow(q, mod, x, e):
+        r = 1
+        while e:
+            if e & 1:
+                r = pyoracle.gf_mul(q, mod, r, x)
+            x = pyoracle.gf_mul(q, mod, x, x)
+            e >>= 1
+        return r
+
+    for q in (1, 2, 7, 8, 16, 31, 32, 63, 64, 80, 127, 128):
+        ctx = bx.field(q)
+        xs = [0, 1] + [rnd.getrandbits(q) for _ in range(6)]
+        es = [0, 5] + [rnd.getrandbits(rnd.choice([3, 40, 130, 300])) for _ in range(6)]
+        for x, e in zip(xs, es):
+            e_ref = e if (e < (1 << q) - 1 or x == 0) else e % ((1 << q) - 1)
+            if x == 0 and e > 0:
+                want = 0
+            else:
+                want = ref_pow(q, ctx.modulus, x, e_ref)
+            assert ctx.pow(x, e) == want, (q, x, e)
+        n0 = _lib.launch_count()
+        x = rnd.getrandbits(q) | 1
+        inv = ctx.inv(x)
+        assert _lib.launch_count() - n0 == 1          # one device launch per inverse
+        assert ctx.mul(x, inv) == 1
+    with pytest.raises(ZeroDivisionError):
+        bx.field(8).inv(0)
+    with pytest.raises(ValueError):
+        bx.field(8).pow(3, -1)
+    # a non-default irreducible modulus: x^8 + x^4 + x^3 + x + 1 (AES)
+    ctx = bx.GFContext(8, 0x11B)
+    for x in range(1, 256):
+        assert pyoracle.gf_mul(8, 0x11B, x, ctx.inv(x)) == 1
+
+
 def test_run_parallel_order_and_errors():
     ctx = bx.field(4)
     rnd = random.Random(14)
@@ -330,15 +373,17 @@ def test_lazy_iteration_matches_run():
     assert sink.getvalue() == coracle.extract_eq(xb, yb, q, n, k)
 
 
-def test_native_pipe_random_push_sizes():
-    """bx_pipe: any sequence of push sizes equals one run over the concatenation."""
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_native_pipe_random_push_sizes(depth):
+    """bx_pipe: any sequence of push sizes equals one run over the concatenation,
+    synchronous (depth 1) and with 1-2 pushes in flight."""
     from paper_2402_14607_b200.pipe import Pipe
-    rnd = random.Random(17)
+    rnd = random.Random(17 + depth)
     for q, n in [(4, 64), (13, 7), (56, 48), (128, 8), (1, 3), (80, 71)]:
         total = rnd.randint(20_000, 120_000)
         xb, yb = rnd.randbytes(total), rnd.randbytes(total)
         out = []
-        with Pipe(q, n, chunk_bytes=9000) as p:
+        with Pipe(q, n, chunk_bytes=9000, depth=depth) as p:
             pos = 0
             while pos < total:
                 step = min(total - pos, rnd.choice([1, 7, 100, 4096, 9000]))
@@ -348,6 +393,38 @@ def test_native_pipe_random_push_sizes():
             k = p.blocks
         assert k == total * 8 // (q * n)
         assert b"".join(out) == coracle.extract_eq(xb, yb, q, n, k), (q, n)
+
+
+def test_native_pipe_async_latency_and_errors():
+    """depth 2: a push returns the previous push's output; capacity and
+    in-flight misuse are reported through bx_last_error."""
+    import ctypes
+
+    from paper_2402_14607_b200 import _lib
+    from paper_2402_14607_b200.pipe import Pipe
+    q, n = 16, 64
+    B = q * n // 8
+    rnd = random.Random(5)
+    xb, yb = rnd.randbytes(8 * B), rnd.randbytes(8 * B)
+    want = coracle.extract_eq(xb, yb, q, n, 8)
+    with Pipe(q, n, chunk_bytes=4 * B, depth=2) as p:
+        assert p.push(xb[:4 * B], yb[:4 * B]) == b""           # push 0 in flight
+        assert p.push(xb[4 * B:], yb[4 * B:]) == want[:len(want) // 2]   # push 0s 4 blocks
+        assert p.flush() == want[len(want) // 2:]
+    L = _lib.lib()
+    h = L.bx_pipe_create_async(q, n, 4 * B, 0, 2)
+    try:
+        got = ctypes.c_int64()
+        one = (ctypes.c_uint8 * 1)()
+        assert L.bx_pipe_push(h, xb, yb, 4 * B, None, 0, ctypes.byref(got)) == 0
+        assert L.bx_pipe_flush(h, one, ctypes.byref(got)) == _lib.BX_EINVAL
+        assert b"drain first" in L.bx_last_error()
+        assert L.bx_pipe_push(h, xb, yb, 4 * B, one, 1, ctypes.byref(got)) == _lib.BX_EINVAL
+        assert b"out_cap" in L.bx_last_error()
+        assert L.bx_pipe_push(h, xb, yb, 5 * B, one, 1, ctypes.byref(got)) == _lib.BX_EINVAL
+        assert b"chunk_bytes" in L.bx_last_error()
+    finally:
+        L.bx_pipe_destroy(h)
 
 
 def test_custom_modulus_contexts():
