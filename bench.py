@@ -399,11 +399,21 @@ def run_ours(args, wls) -> None:
     from paper_2402_14607_b200 import workloads as W
 
     world, rank, local = _dist()
+    # BX_BENCH_ONE_GPU=1 maps every rank to device 0: a FUNCTIONAL check of the
+    # N>1 path (sharding, IPC output sharing, fused peer-store gather, parity)
+    # on a one-GPU box; its timings are not scaling numbers (flagged in config)
+    one_gpu = os.environ.get("BX_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     use_dist = "RANK" in os.environ and "WORLD_SIZE" in os.environ   # launched by torchrun
     if use_dist:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")     # NCCL refuses two ranks on one GPU
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if one_gpu else dev
     strong = args.scaling == "strong" or world == 1
     b = wls[0].b
 
@@ -514,7 +524,7 @@ def run_ours(args, wls) -> None:
     launches = _lib.launch_count() - launches0
     ko_ms, ko_per = (timed(True, args.steps) if locals_ is not None else (ms, per))
     if use_dist:
-        t = torch.tensor([ms, ko_ms, *per, *ko_per], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms, ko_ms, *per, *ko_per], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         v = t.tolist()
         ms, ko_ms, per, ko_per = v[0], v[1], v[2:2 + len(wls)], v[2 + len(wls):]
@@ -583,7 +593,7 @@ def run_ours(args, wls) -> None:
     except Exception as exc:  # noqa: BLE001 - reported in the JSON line
         e2e_err = repr(exc)
     if use_dist:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
@@ -615,7 +625,9 @@ def run_ours(args, wls) -> None:
                                        "over CUDA IPC (fused gather, no collective)"
                                        if strong and world > 1 else
                                        f"dp{world}: independent replicas" if world > 1 else "1 GPU"),
-                       "note": wls[0].note},
+                       "note": wls[0].note,
+                       **({"functional_only": "BX_BENCH_ONE_GPU=1: all ranks on device 0, "
+                                              "not a scaling measurement"} if one_gpu else {})},
             "output_gbps": out_gbps,
             "raw_gbps_per_gpu": raw_gbps / world,
             "output_gbps_per_gpu": out_gbps / world,

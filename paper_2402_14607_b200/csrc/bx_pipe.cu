@@ -25,10 +25,16 @@
 // push k's kernel and D2H; depth 1 is the synchronous pipe (every push
 // returns its own output).  bx_pipe_drain retires everything in flight.
 #include <algorithm>
+#include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <new>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -67,6 +73,78 @@ struct DevGuard {
   }
 };
 
+// Host copy workers: the staging memcpy (caller memory -> pinned slot) is
+// host-memory bound at ~10 GB/s per thread, so each push splits its x and y
+// copies into pieces run by a few persistent threads (BX_PIPE_THREADS,
+// default 4) plus the calling thread.
+class CopyPool {
+ public:
+  explicit CopyPool(int n) {
+    for (int i = 0; i < n; i++) th_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> l(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  // copies every (dst, src, len) job; returns when all are done
+  void run(const std::vector<std::tuple<uint8_t*, const uint8_t*, size_t>>& jobs) {
+    {
+      std::lock_guard<std::mutex> l(m_);
+      jobs_ = &jobs;
+      next_ = 0;
+      left_ = jobs.size();
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> l(m_);
+    done_.wait(l, [this] { return left_ == 0; });
+    jobs_ = nullptr;
+  }
+
+ private:
+  bool take(size_t* i) {
+    std::lock_guard<std::mutex> l(m_);
+    if (!jobs_ || next_ >= jobs_->size()) return false;
+    *i = next_++;
+    return true;
+  }
+  void work() {
+    size_t i;
+    while (take(&i)) {
+      auto [d, s, n] = (*jobs_)[i];
+      std::memcpy(d, s, n);
+      std::lock_guard<std::mutex> l(m_);
+      if (--left_ == 0) done_.notify_all();
+    }
+  }
+  void loop() {
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> l(m_);
+        cv_.wait(l, [this] { return stop_ || (jobs_ && next_ < jobs_->size()); });
+        if (stop_) return;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::vector<std::tuple<uint8_t*, const uint8_t*, size_t>>* jobs_ = nullptr;
+  size_t next_ = 0, left_ = 0;
+  bool stop_ = false;
+};
+
+int pipe_threads() {
+  const char* e = std::getenv("BX_PIPE_THREADS");
+  const int n = e ? std::atoi(e) : 4;
+  return std::max(0, std::min(n, 32));
+}
+
 int cuda_fail(const char* what, cudaError_t e) {
   return bx::set_error(BX_ECUDA, std::string("bx_pipe: ") + what + ": " + cudaGetErrorString(e));
 }
@@ -91,6 +169,7 @@ struct bx_pipe {
   int out_carry_bits = 0;      // valid bits in dcarry
   int64_t blocks_done = 0;
   cudaStream_t cx = nullptr, cy = nullptr, comp = nullptr;
+  CopyPool* pool = nullptr;
 };
 
 namespace {
@@ -107,6 +186,8 @@ void release(bx_pipe* p) {
     if (s.ey) cudaEventDestroy(s.ey);
     if (s.done) cudaEventDestroy(s.done);
   }
+  delete p->pool;
+  p->pool = nullptr;
   cudaFree(p->dcarry);
   if (p->cx) cudaStreamDestroy(p->cx);
   if (p->cy) cudaStreamDestroy(p->cy);
@@ -174,6 +255,10 @@ bx_pipe* bx_pipe_create_async(int q, int n, int64_t chunk_bytes, int device, int
       ok(cudaStreamCreateWithFlags(&p->cx, cudaStreamNonBlocking)) &&
       ok(cudaStreamCreateWithFlags(&p->cy, cudaStreamNonBlocking)) &&
       ok(cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking));
+  if (e == cudaSuccess) {
+    const int nt = pipe_threads();
+    if (nt > 0) p->pool = new (std::nothrow) CopyPool(nt);
+  }
   if (e != cudaSuccess) {
     cuda_fail("create", e);
     release(p);
@@ -217,6 +302,23 @@ int bx_pipe_push(bx_pipe* p, const void* x, const void* y, int64_t nbytes, void*
   // previous push's slot, never this one (nslots >= 2)
   cudaError_t e;
   const int64_t rest = p->carry_bytes;
+  if (nbytes) {
+    // stage both streams into the slot's pinned buffers: pieces of >= 1 MiB
+    // over the copy workers
+    std::vector<std::tuple<uint8_t*, const uint8_t*, size_t>> jobs;
+    const int64_t piece = std::max<int64_t>(1 << 20, nbytes / (2 * (p->pool ? 5 : 1)) + 1);
+    for (int side = 0; side < 2; side++) {
+      uint8_t* h = side ? s.hy : s.hx;
+      const uint8_t* src = static_cast<const uint8_t*>(side ? y : x);
+      for (int64_t o = 0; o < nbytes; o += piece)
+        jobs.emplace_back(h + o, src + o, (size_t)std::min(piece, nbytes - o));
+    }
+    if (p->pool && jobs.size() > 1) {
+      p->pool->run(jobs);
+    } else {
+      for (auto& [d, src, len] : jobs) std::memcpy(d, src, len);
+    }
+  }
   for (int side = 0; side < 2; side++) {
     uint8_t* dst = side ? s.dy : s.dx;
     uint8_t* h = side ? s.hy : s.hx;
@@ -227,7 +329,6 @@ int bx_pipe_push(bx_pipe* p, const void* x, const void* y, int64_t nbytes, void*
         return cuda_fail("carry tail", e);
     }
     if (nbytes) {
-      std::memcpy(h, side ? y : x, (size_t)nbytes);
       if ((e = cudaMemcpyAsync(dst + rest, h, nbytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
         return cuda_fail("H2D", e);
     }
