@@ -389,6 +389,12 @@ def _gen_streams(wls, start_sample: int, count: int, dev, seed_shift: int):
     return out
 
 
+def _trace(rank: int, what: str) -> None:
+    """BX_BENCH_TRACE=1: per-rank stage markers on stderr (diagnosing N>1 runs)."""
+    if os.environ.get("BX_BENCH_TRACE") == "1":
+        print(f"[bench rank {rank} {time.strftime('%H:%M:%S')}] {what}", file=sys.stderr, flush=True)
+
+
 def run_ours(args, wls) -> None:
     import numpy as np
     import torch
@@ -407,6 +413,11 @@ def run_ours(args, wls) -> None:
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    _trace(rank, "init")
+    if os.environ.get("BX_BENCH_TRACE") == "1":
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ.get("BX_BENCH_TRACE_AFTER", "150")),
+                                          exit=False)
     use_dist = "RANK" in os.environ and "WORLD_SIZE" in os.environ   # launched by torchrun
     if use_dist:
         if one_gpu:
@@ -422,6 +433,7 @@ def run_ours(args, wls) -> None:
               for wl in wls]
     lo_s = min(s * wl.block_bits // b for wl, (s, c) in zip(wls, ranges))
     hi_s = max(-(-((s + c) * wl.block_bits) // b) for wl, (s, c) in zip(wls, ranges))
+    _trace(rank, "gen")
     t_gen = time.perf_counter()
     (xd, xn, xh), (yd, yn, yh) = _gen_streams(wls, lo_s, hi_s - lo_s, dev,
                                               0 if strong else 1000 * rank)
@@ -441,6 +453,7 @@ def run_ours(args, wls) -> None:
         dist.broadcast_object_list(shared, src=0)
         if rank != 0:
             outs = [fn(*a) for fn, a in shared[0]]
+    _trace(rank, "outputs")
     locals_ = ([torch.zeros(D.padded_len((c * wl.q + 7) // 8 + 8), dtype=torch.uint8, device=dev)
                 for wl, (s, c) in zip(wls, ranges)] if world > 1 and strong else None)
     stream = torch.cuda.current_stream(dev)
@@ -490,6 +503,7 @@ def run_ours(args, wls) -> None:
     if use_dist:
         dist.barrier()
 
+    _trace(rank, "parity")
     # ---- parity: sampled blocks of every leg's gathered output (rank 0 holds
     # the whole job) vs the oracle on windows regenerated on the host
     mism, checked = 0, 0
@@ -517,6 +531,7 @@ def run_ours(args, wls) -> None:
         except Exception as exc:  # noqa: BLE001 - recorded, not fatal
             mism = f"parity check failed to run: {exc!r}"
 
+    _trace(rank, "timed")
     # ---- timed region
     sampler = ClockSampler(local)
     launches0 = _lib.launch_count()
@@ -555,6 +570,7 @@ def run_ours(args, wls) -> None:
     for s in sweep:
         del s["roofline"]["launch"]
 
+    _trace(rank, "e2e")
     # ---- e2e: the public API from pinned host memory, every step (H2D of the
     # inputs, kernels, D2H of the gathered output to rank 0's host)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
@@ -592,11 +608,14 @@ def run_ours(args, wls) -> None:
                          for r, o, ob in zip(res, outs, obytes))
     except Exception as exc:  # noqa: BLE001 - reported in the JSON line
         e2e_err = repr(exc)
+        import traceback
+        _trace(rank, "e2e failed:\n" + traceback.format_exc())
     if use_dist:
         t = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    _trace(rank, "cpu")
     # ---- CPU baselines (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

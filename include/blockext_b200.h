@@ -91,6 +91,20 @@ int bx_launch_info(int q, int n, int64_t nblocks, int* tpb, int* tile, int* stag
                    int* threads, int* smem_bytes, int64_t* grid, int* family);
 
 /*
+ * One-call extraction of a short run from HOST memory (the real-time path:
+ * one call per capture chunk): reads bytes [0, ceil((x_bit0 + nblocks*q*n)/8))
+ * of x (x_bytes = what the caller can provide; must cover that) and likewise
+ * y, stages both through a per-device cached pinned buffer, copies them to
+ * `device` with one H2D, runs bx_extract_eq and writes the packed output --
+ * ceil(nblocks*q/8) bytes, last byte zero-padded -- to host memory `out`.
+ * Synchronous; thread-safe (calls on one device are serialised).  For long
+ * runs use bx_extract_eq on device buffers with your own copy pipeline.
+ */
+int bx_extract_eq_host(const void* x, int64_t x_bytes, int64_t x_bit0, const void* y,
+                       int64_t y_bytes, int64_t y_bit0, int q, int n, int64_t nblocks,
+                       void* out, int device);
+
+/*
  * Sample packer: the low b bits of sample i go to stream bits
  * [out_bit0 + i*b, out_bit0 + (i+1)*b).  samples: `count` little-endian
  * unsigned integers of elem_bytes (1, 2, 4 or 8) each; b in 1..8*elem_bytes.

@@ -13,6 +13,7 @@ reference, so reports compare equal float-for-float.
 """
 from __future__ import annotations
 
+import functools
 import math
 from dataclasses import dataclass
 from fractions import Fraction
@@ -140,6 +141,19 @@ def _check_b(b: int) -> None:
 
 def error_bound_block(vec_len: int, field_bits: int, entropy_rate) -> float:
     """log2(sqrt 3) - 1/4 - (rate/4 - 1/8)*q*n + 2q, fixed evaluation order."""
+    if isinstance(entropy_rate, Fraction):
+        # the hashable common case: memoised (a streaming caller evaluates the
+        # same plan's bound once per call)
+        return _error_bound_block_cached(vec_len, field_bits, entropy_rate)
+    return _error_bound_block(vec_len, field_bits, entropy_rate)
+
+
+@functools.lru_cache(maxsize=256)
+def _error_bound_block_cached(vec_len: int, field_bits: int, entropy_rate: Fraction) -> float:
+    return _error_bound_block(vec_len, field_bits, entropy_rate)
+
+
+def _error_bound_block(vec_len: int, field_bits: int, entropy_rate) -> float:
     rate = as_rational(entropy_rate, "entropy_rate")
     if vec_len < 1 or field_bits < 1:
         raise ValueError("vec_len and field_bits must be >= 1")

@@ -260,6 +260,13 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
     xn, yn = (x_bit0 + count * B + 7) // 8, (y_bit0 + count * B + 7) // 8
     obytes = (count * q + 7) // 8
     if not (xt.is_cuda or yt.is_cuda) and xn + yn <= SMALL_INPUT_BYTES:
+        if dev_out is None and xt.is_contiguous() and yt.is_contiguous():
+            # one C call: staging, H2D, kernel, D2H, synchronise
+            from . import _lib
+            _lib.check(_lib.lib().bx_extract_eq_host(
+                xt.data_ptr(), xt.numel(), x_bit0, yt.data_ptr(), yt.numel(), y_bit0, q, n, count,
+                out.data_ptr() + out_byte0, dev.index), "bx_extract_eq_host")
+            return
         res, rbit = dev_out if dev_out is not None else (None, 0)
         with torch.cuda.device(dev):
             _SmallPath.get(dev).run(xt, yt, xn, yn, q, n, count, x_bit0, y_bit0,
@@ -380,7 +387,10 @@ def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit
     B = q * n
     obytes = (count * q + 7) // 8
     if out is None:
-        out = torch.empty(obytes, dtype=torch.uint8, pin_memory=True)
+        # small host runs come back through bx_extract_eq_host's own pinned
+        # staging (a memcpy), so their result needs no pinned allocation
+        small = len(devs) == 1 and 2 * ((x_bit0 + count * B + 7) // 8) <= SMALL_INPUT_BYTES
+        out = torch.empty(obytes, dtype=torch.uint8, pin_memory=not small)
     else:
         out = out[:obytes]
     ranges = [r for r in shard_ranges(count, len(devs)) if r[1] > 0]
@@ -435,7 +445,8 @@ def distributed_extract(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0,
     """
     if gather == "peer":
         return _distributed_extract_peer(xv, yv, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0,
-                                         group=group, device=device, to_host=to_host)
+                                         group=group, device=device, to_host=to_host,
+                                         local_input=local_input)
     if gather != "object":
         raise ValueError(f"unknown gather mode {gather!r}")
     import torch.distributed as dist
@@ -487,18 +498,36 @@ def _distributed_extract_peer(xv, yv, q: int, n: int, count: int, *, x_bit0: int
         buf = rebuild(*args)              # rank 0's buffer mapped into this process
     start, cnt = rank_range(count, rank, world)
     B = q * n
-    if cnt:
-        xs, ys = (x_bit0, y_bit0) if local_input else (x_bit0 + start * B, y_bit0 + start * B)
-        _extract_one_device(_slice(xv, xs // 8, (xs + cnt * B + 7) // 8),
-                            _slice(yv, ys // 8, (ys + cnt * B + 7) // 8),
-                            q, n, cnt, xs % 8, ys % 8, dev, None, 0,
-                            dev_out=(buf, start * q))
-    torch.cuda.synchronize(dev)
+    failure = None
+    try:
+        if cnt:
+            xs, ys = (x_bit0, y_bit0) if local_input else (x_bit0 + start * B, y_bit0 + start * B)
+            _extract_one_device(_slice(xv, xs // 8, (xs + cnt * B + 7) // 8),
+                                _slice(yv, ys // 8, (ys + cnt * B + 7) // 8),
+                                q, n, cnt, xs % 8, ys % 8, dev, None, 0,
+                                dev_out=(buf, start * q))
+        torch.cuda.synchronize(dev)
+    except Exception as exc:  # noqa: BLE001 - re-raised after the barrier protocol
+        failure = exc
+    # the barriers run on every rank whatever happened above, so a failing
+    # rank cannot leave the others waiting in a collective; every rank then
+    # learns whether any range failed
     dist.barrier(group=group)           # every range is in rank 0's buffer
+    flag = torch.tensor([0 if failure is None else 1], dtype=torch.int32,
+                        device=dev if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(flag, group=group)
     if rank != 0:
         del buf
         dist.barrier(group=group)       # rank 0 may free the buffer after this
+        if failure is not None:
+            raise failure
+        if int(flag.item()):
+            raise RuntimeError("distributed_extract: another rank's range failed")
         return None
     dist.barrier(group=group)
+    if failure is not None:
+        raise failure
+    if int(flag.item()):
+        raise RuntimeError("distributed_extract: another rank's range failed")
     res = buf[:obytes]
     return res.cpu().numpy().tobytes() if to_host else res

@@ -46,6 +46,17 @@ def main():
                                            st.synchronize()))
     res["h2d_128KiB_pinned_sync"] = med(lambda: (xd[:xn].copy_(hp, non_blocking=True), st.synchronize()))
     res["zero_plus_sync"] = med(lambda: (out.zero_(), st.synchronize()))
+    from paper_2402_14607_b200 import _lib
+    L = _lib.lib()
+    xa = np.frombuffer(x1, np.uint8)
+    ya = np.frombuffer(y1, np.uint8)
+    oa = np.empty(k * q // 8, np.uint8)
+    res["c_host_call"] = med(lambda: L.bx_extract_eq_host(xa.ctypes.data, xa.size, 0, ya.ctypes.data,
+                                                          ya.size, 0, q, n, k, oa.ctypes.data, 0))
+    xq, yq = x1[:4096 * 4], y1[:4096 * 4]          # 1/8 of the bytes: the copy share
+    res["c_host_call_eighth"] = med(lambda: L.bx_extract_eq_host(
+        np.frombuffer(xq, np.uint8).ctypes.data, len(xq), 0, np.frombuffer(yq, np.uint8).ctypes.data,
+        len(yq), 0, q, n, k // 8, oa.ctypes.data, 0))
     res["extract_packed"] = med(lambda: sharding.extract_packed(x1, y1, q, n, k))
     res["api_run"] = med(lambda: bx.extract_eq(x1, y1, plan).run(io.BytesIO()))
     print(json.dumps(res))
