@@ -105,6 +105,19 @@ int bx_extract_eq_host(const void* x, int64_t x_bytes, int64_t x_bit0, const voi
                        void* out, int device);
 
 /*
+ * Extension beyond the reference's q <= 128 cap (its GFContext raises
+ * CapacityError above 128, gf2q.py:111-112): equal-width blocks over
+ * GF(2^256) with P = x^256 + x^10 + x^5 + x^2 + 1 (the first irreducible of
+ * the reference's modulus scan order, _moduli.py:1-11), for BASELINE config 3
+ * as stated (1024-bit blocks -> 256 output bits: q = 256, n = 4).  Block l
+ * reads bytes [32*n*l, 32*n*(l+1)) of x and y (16-byte aligned) and writes
+ * words [out_word0 + 8*l, +8) of out (whole 32-bit words; out + 4*out_word0
+ * 16-byte aligned).  q must be 256 (BX_ERANGE otherwise).
+ */
+int bx_extract_eq_wide(const void* x, int64_t x_bytes, const void* y, int64_t y_bytes, int q,
+                       int n, int64_t nblocks, void* out, int64_t out_word0, void* stream);
+
+/*
  * Sample packer: the low b bits of sample i go to stream bits
  * [out_bit0 + i*b, out_bit0 + (i+1)*b).  samples: `count` little-endian
  * unsigned integers of elem_bytes (1, 2, 4 or 8) each; b in 1..8*elem_bytes.

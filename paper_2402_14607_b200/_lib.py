@@ -40,6 +40,7 @@ SIGNATURES = {
     "bx_pipe_flush": (_i32, [_vp, _vp, _PI64]),
     "bx_pipe_create_async": (_vp, [_i32, _i32, _i64, _i32, _i32]),
     "bx_gf_pow": (_i32, [_i32, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "bx_extract_eq_wide": (_i32, [_vp, _i64, _vp, _i64, _i32, _i32, _i64, _vp, _i64, _vp]),
     "bx_extract_eq_host": (_i32, [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i64, _vp, _i32]),
     "bx_pipe_drain": (_i32, [_vp, _vp, _i64, _PI64]),
     "bx_pipe_max_output": (_i64, [_vp]),

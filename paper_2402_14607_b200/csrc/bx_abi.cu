@@ -23,6 +23,7 @@ cudaError_t launch_ip_table(int, uint32_t, int, uint32_t, uint32_t, uint16_t*, c
 cudaError_t launch_ip_hist(int, uint32_t, int, uint32_t, uint32_t, uint32_t*, cudaStream_t);
 cudaError_t launch_rows_uniform(const uint32_t*, uint32_t, uint32_t, uint32_t, uint8_t*,
                                 cudaStream_t);
+cudaError_t launch_wide256(const void*, const void*, int, int64_t, void*, cudaStream_t);
 cudaError_t launch_gf_pow(int, const uint32_t*, const uint32_t*, const uint32_t*, int64_t, uint32_t*,
                           cudaStream_t);
 cudaError_t launch_gf_ip_generic(int, const uint32_t*, const uint32_t*, const uint32_t*, int, int64_t,
@@ -353,6 +354,29 @@ int bx_rows_uniform(const void* counts, uint32_t nrows, uint32_t bins, uint32_t 
   cudaError_t e = bx::launch_rows_uniform(static_cast<const uint32_t*>(counts), nrows, bins, expected,
                                           static_cast<uint8_t*>(flags), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_rows_uniform: ") + cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return BX_OK;
+}
+
+int bx_extract_eq_wide(const void* x, int64_t x_bytes, const void* y, int64_t y_bytes, int q, int n,
+                       int64_t nblocks, void* out, int64_t out_word0, void* stream) {
+  if (q != 256) return fail(BX_ERANGE, "wide extraction supports q = 256");
+  if (n < 1 || nblocks < 0 || x_bytes < 0 || y_bytes < 0 || out_word0 < 0)
+    return fail(BX_EINVAL, "bad wide shape");
+  if (nblocks == 0) return BX_OK;
+  if (!x || !y || !out) return fail(BX_EINVAL, "null buffer");
+  if ((((uintptr_t)x) | ((uintptr_t)y)) & 15) return fail(BX_EINVAL, "x and y must be 16-byte aligned");
+  if ((((uintptr_t)out) + 4 * out_word0) & 15)
+    return fail(BX_EINVAL, "out + 4*out_word0 must be 16-byte aligned");
+  if (nblocks > INT64_MAX / (32 * (int64_t)n)) return fail(BX_EINVAL, "block range overflows");
+  const int64_t need = nblocks * 32 * (int64_t)n;
+  if (need > x_bytes || need > y_bytes) return fail(BX_EINVAL, "stream shorter than the block range");
+  const DeviceScope scope(x, stream);
+  if (!scope.reaches(y) || !scope.reaches(out))
+    return fail(BX_EINVAL, "y or out lives on a GPU x's device cannot reach");
+  cudaError_t e = bx::launch_wide256(x, y, n, nblocks, static_cast<uint32_t*>(out) + out_word0,
+                                     static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(BX_ECUDA, std::string("bx_extract_eq_wide: ") + cudaGetErrorString(e));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return BX_OK;
 }

@@ -78,6 +78,54 @@ int main(void) {
     bx_pipe_destroy(p);
     free(hx); free(hy); free(got); free(want);
   }
+  /* async pipe (2 pushes in flight) + drain + flush: same bytes as one run */
+  {
+    const int q = 16, n = 64;
+    const int64_t total = 2000003, chunk = 1 << 19;
+    uint8_t *hx = malloc(total), *hy = malloc(total), *want = calloc(total, 1);
+    for (int64_t i = 0; i < total; i++) { hx[i] = rb(); hy[i] = rb(); }
+    bx_pipe* p = bx_pipe_create_async(q, n, chunk, 0, 2);
+    const int64_t cap = 2 * bx_pipe_max_output(p);
+    uint8_t* got = calloc(total + cap, 1);
+    int64_t pos = 0, outpos = 0, got_bytes = 0;
+    while (pos < total) {
+      int64_t step = (pos / 4099) % 2 ? 7777 : chunk;
+      if (step > total - pos) step = total - pos;
+      if (bx_pipe_push(p, hx + pos, hy + pos, step, got + outpos, cap, &got_bytes)) {
+        printf("async push: %s\n", bx_last_error()); fails++; break;
+      }
+      pos += step; outpos += got_bytes;
+    }
+    if (bx_pipe_drain(p, got + outpos, cap, &got_bytes)) fails++;
+    outpos += got_bytes;
+    bx_pipe_flush(p, got + outpos, &got_bytes); outpos += got_bytes;
+    const int64_t k = bx_pipe_blocks(p);
+    int exps[5];
+    int ne = bx_modulus_exponents(q, exps);
+    bxo_extract_eq(hx, 0, hy, 0, q, n, k, exps, ne, want, 0, 1, 1);
+    const int ok = k == total * 8 / (q * n) && outpos == (k * q + 7) / 8 && memcmp(got, want, outpos) == 0;
+    printf("async pipe q=%d n=%d blocks=%lld: %s\n", q, n, (long long)k, ok ? "ok" : "MISMATCH");
+    fails += !ok;
+    bx_pipe_destroy(p);
+    free(hx); free(hy); free(got); free(want);
+  }
+  /* one-call host extraction at a bit offset (config-1 shape) */
+  {
+    const int q = 32, n = 4;
+    const int64_t k = 8192, bit0 = 5;
+    const int64_t bytes = (bit0 + k * q * n + 7) / 8;
+    uint8_t *hx = malloc(bytes), *hy = malloc(bytes), *got = calloc(k * q / 8, 1), *want = calloc(k * q / 8 + 16, 1);
+    for (int64_t i = 0; i < bytes; i++) { hx[i] = rb(); hy[i] = rb(); }
+    int rc = bx_extract_eq_host(hx, bytes, bit0, hy, bytes, bit0, q, n, k, got, 0);
+    int exps[5];
+    int ne = bx_modulus_exponents(q, exps);
+    bxo_extract_eq(hx, bit0, hy, bit0, q, n, k, exps, ne, want, 0, 1, 1);
+    const int ok = rc == 0 && memcmp(got, want, k * q / 8) == 0;
+    printf("host one-call q=%d n=%d blocks=%lld: %s\n", q, n, (long long)k, ok ? "ok" : "MISMATCH");
+    fails += !ok;
+    if (bx_extract_eq_host(hx, bytes - 1, bit0, hy, bytes, bit0, q, n, k, got, 0) != BX_EINVAL) fails++;
+    free(hx); free(hy); free(got); free(want);
+  }
   /* error path: field width beyond the cap */
   if (bx_extract_eq(NULL, 0, 0, NULL, 0, 0, 200, 4, 1, NULL, 0, NULL) != BX_ERANGE) fails++;
   printf("launches=%lld version=%d fails=%d\n", (long long)bx_launch_count(0), bx_version(), fails);

@@ -1,0 +1,14 @@
+# round-2 measurement pass: default bench line, launch list, ncu --set full of every C5 leg kernel
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit,temperature.gpu --format=csv
+timeout 300 python tools/api_overhead.py > gpurun_out/api_overhead.json 2> gpurun_out/api_overhead.err
+timeout 900 python bench.py > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+echo "bench rc=$?"
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+echo "ref rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1 --e2e-warmup 0 > gpurun_out/ncu_launch.log 2>&1
+echo "launch rc=$?"
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:eq_direct_kernel -s 15 -c 5 -o gpurun_out/ncu_c5_r02 -f python bench.py --steps 1 --warmup 3 --no-cpu --e2e-steps 1 --e2e-warmup 0 > gpurun_out/ncu_full.log 2>&1
+echo "ncu rc=$?"
+cat gpurun_out/api_overhead.json; tail -c 400 gpurun_out/bench_c5.json; tail -c 300 gpurun_out/bench_ref.json; tail -3 gpurun_out/ncu_full.log
