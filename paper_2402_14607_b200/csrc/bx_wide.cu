@@ -118,7 +118,11 @@ __device__ __forceinline__ void reduce256(const uint32_t (&c)[16], uint32_t (&z)
   // spill < 2^10, so spill << 10 < 2^20: no further overflow
 }
 
-__global__ void __launch_bounds__(128) eq_wide256_kernel(const uint4* __restrict__ x,
+#ifndef BX_WIDE_MINB
+#define BX_WIDE_MINB 1
+#endif
+
+__global__ void __launch_bounds__(128, BX_WIDE_MINB) eq_wide256_kernel(const uint4* __restrict__ x,
                                                          const uint4* __restrict__ y, int n,
                                                          int64_t nblocks, uint32_t* __restrict__ out) {
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
