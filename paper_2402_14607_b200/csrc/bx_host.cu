@@ -4,7 +4,8 @@
 //
 // bx_extract_eq_host stages both windows into a per-device cached pinned
 // buffer, moves them with ONE H2D, runs bx_extract_eq, brings the packed output
-// back with one D2H and synchronises: four stream operations and no
+// back with one D2H and synchronises: three stream operations (the zeroed
+// output region rides in the H2D) and no
 // allocation after the first call, so a config-1 run (2 x 128 KiB) costs the
 // copies plus a few microseconds of API time instead of a Python/torch
 // orchestration of each step.
@@ -109,11 +110,10 @@ extern "C" int bx_extract_eq_host(const void* x, int64_t x_bytes, int64_t x_bit0
   std::memset(h + xn, 0, (size_t)(px - xn));
   std::memcpy(h + px, y, (size_t)yn);
   std::memset(h + px + yn, 0, (size_t)(py - yn));
+  std::memset(h + px + py, 0, (size_t)po);   // the zeroed output rides along in the one H2D
   uint8_t* d = c->d;
-  if ((e = cudaMemcpyAsync(d, h, (size_t)(px + py), cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
+  if ((e = cudaMemcpyAsync(d, h, (size_t)(px + py + po), cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
     return cuda_fail("H2D", e);
-  if ((e = cudaMemsetAsync(d + px + py, 0, (size_t)po, c->st)) != cudaSuccess)
-    return cuda_fail("memset", e);
   const int rc = bx_extract_eq(d, xn, x_bit0, d + px, yn, y_bit0, q, n, nblocks, d + px + py, 0, c->st);
   if (rc) return rc;
   if ((e = cudaMemcpyAsync(h + px + py, d + px + py, (size_t)ob, cudaMemcpyDeviceToHost, c->st)) !=

@@ -370,6 +370,44 @@ def extract_neq_packed(xv, yv, q1: int, step: int, n: int, count: int, *, device
         return res[:(total_out + 7) // 8].cpu().numpy().tobytes()
 
 
+def _host_array(buf):
+    """Zero-copy uint8 numpy view of a host buffer (None for CUDA tensors)."""
+    if isinstance(buf, np.ndarray):
+        return np.ascontiguousarray(buf).reshape(-1).view(np.uint8)
+    if isinstance(buf, (bytes, bytearray, memoryview)):
+        return np.frombuffer(memoryview(buf).cast("B"), dtype=np.uint8)
+    try:
+        import torch
+        if isinstance(buf, torch.Tensor) and not buf.is_cuda:
+            return buf.reshape(-1).view(torch.uint8).numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    return None
+
+
+def extract_small(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit0: int = 0,
+                  device=None):
+    """Packed output of a short run from host memory through one C call
+    (bx_extract_eq_host), or None when the inputs are not plain host buffers
+    or the run is too large for the one-shot path."""
+    from . import _lib
+    from . import device as D
+
+    xa, ya = _host_array(xv), _host_array(yv)
+    if xa is None or ya is None:
+        return None
+    B = q * n
+    xn, yn = (x_bit0 + count * B + 7) // 8, (y_bit0 + count * B + 7) // 8
+    if xn + yn > SMALL_INPUT_BYTES or xa.size < xn or ya.size < yn:
+        return None
+    dev = D.require_cuda(device)
+    out = np.empty((count * q + 7) // 8, dtype=np.uint8)
+    _lib.check(_lib.lib().bx_extract_eq_host(xa.ctypes.data, xa.size, x_bit0, ya.ctypes.data,
+                                             ya.size, y_bit0, q, n, count, out.ctypes.data,
+                                             dev.index), "bx_extract_eq_host")
+    return out
+
+
 def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit0: int = 0,
                    device=None, devices=None, out=None) -> np.ndarray:
     """Packed output of `count` blocks (uint8 array over pinned memory; the last
@@ -380,6 +418,13 @@ def extract_packed(xv, yv, q: int, n: int, count: int, *, x_bit0: int = 0, y_bit
     of at least ceil(count*q/8) bytes, ideally pinned) receives the bytes
     instead of a fresh pinned buffer."""
     from . import device as D
+
+    if out is None and not (devices and len(devices) > 1):
+        # short host runs: one C call (bx_extract_eq_host), no torch orchestration
+        small = extract_small(xv, yv, q, n, count, x_bit0=x_bit0, y_bit0=y_bit0,
+                              device=devices[0] if devices else device)
+        if small is not None:
+            return small
 
     import torch
 
