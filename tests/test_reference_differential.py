@@ -129,3 +129,50 @@ def test_plans_and_bounds_against_reference(data):
     assert n1.__dict__ == n2.__dict__
     k = data.draw(st.integers(1, 40))
     assert R.error_bound_neq(n1, k) == bx.error_bound_neq(n2, k)
+
+
+class _Recorder(io.BytesIO):
+    """BytesIO that records every read(size) call."""
+
+    def __init__(self, data):
+        super().__init__(data)
+        self.sizes = []
+
+    def read(self, size=-1):
+        self.sizes.append(size)
+        return super().read(size)
+
+
+@settings(max_examples=80, deadline=None)
+@given(st.data())
+def test_bitio_against_reference(data):
+    """BitReader / BitWriter / unpack_values (reference bitio.py:16-108): same
+    values, same read(size) sequence, same counters and tails."""
+    from paper_2402_14607_b200 import bitio as B
+    from blockext import bitio as RB
+
+    raw = data.draw(st.binary(min_size=0, max_size=600))
+    chunk = data.draw(st.sampled_from([1, 3, 16, 64, 1 << 16]))
+    widths = data.draw(st.lists(st.integers(1, 200), min_size=1, max_size=40))
+    a, b = _Recorder(raw), _Recorder(raw)
+    ra, rb = B.BitReader(a, chunk), RB.BitReader(b, chunk)
+    for w in widths:
+        assert ra.read_bits(w) == rb.read_bits(w)
+        assert (ra.bits_consumed, ra.tail_bits()) == (rb.bits_consumed, rb.tail_bits())
+    assert a.sizes == b.sizes
+    wa, wb = B.BitWriter(), RB.BitWriter()
+    for w in widths:
+        v = data.draw(st.integers(0, (1 << w) - 1))
+        wa.write_bits(v, w)
+        wb.write_bits(v, w)
+        assert wa.bit_length == wb.bit_length
+    assert wa.getvalue() == wb.getvalue()
+    width = data.draw(st.integers(1, 128))
+    count = data.draw(st.integers(0, 8 * len(raw) // width + 2))
+    try:
+        want = RB.unpack_values(raw, width, count)
+    except ValueError:
+        with pytest.raises(ValueError):
+            B.unpack_values(raw, width, count)
+    else:
+        assert B.unpack_values(raw, width, count) == want
