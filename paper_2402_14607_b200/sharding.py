@@ -241,6 +241,22 @@ class _SmallPath:
             st.synchronize()   # staging and device buffers are reused by the next call
 
 
+_STREAMS: dict = {}
+_STREAMS_LOCK = threading.Lock()
+
+
+def _copy_streams(dev):
+    """(x copy, y copy, output copy) streams of a device, created once per
+    process (stream creation costs tens of microseconds per call)."""
+    import torch
+
+    with _STREAMS_LOCK:
+        st = _STREAMS.get(dev.index)
+        if st is None:
+            st = _STREAMS[dev.index] = tuple(torch.cuda.Stream(dev) for _ in range(3))
+        return st
+
+
 def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0: int, dev,
                         out, out_byte0: int, dev_out=None) -> None:
     """`count` blocks on one device.  Host inputs are streamed in ~64 MiB chunks
@@ -292,13 +308,12 @@ def _extract_one_device(xv, yv, q: int, n: int, count: int, x_bit0: int, y_bit0:
             # the compute stream runs each chunk as soon as both halves landed;
             # pageable inputs are first staged through pinned rings by run-ahead
             # host threads (see _Stager) so their H2D is asynchronous too
-            cx = torch.cuda.Stream(dev)
-            cy = torch.cuda.Stream(dev)
+            cx, cy, co_cached = _copy_streams(dev)
             # each chunk's output words go back on their own stream as soon as
             # the chunk's kernel finished (D2H overlaps the next chunks' H2D:
             # PCIe is full duplex); chunk boundaries sit on multiples of 64
             # blocks, i.e. on whole output words, so chunks never share a word
-            co = torch.cuda.Stream(dev) if dev_out is None and out.is_pinned() else None
+            co = co_cached if dev_out is None and out.is_pinned() else None
             slot = int(os.environ.get("BX_STAGE_MB", "128")) << 20
             step = max(ALIGN_BLOCKS, (PIPE_CHUNK_BYTES * 8 // B) // ALIGN_BLOCKS * ALIGN_BLOCKS)
             if not pinned:
