@@ -416,6 +416,8 @@ int64_t bx_pipe_blocks(const bx_pipe* p) { return p ? p->blocks_done : -1; }
 void bx_pipe_destroy(bx_pipe* p) {
   if (!p) return;
   DevGuard g(p->device);
+  cudaStreamSynchronize(p->cx);
+  cudaStreamSynchronize(p->cy);
   cudaStreamSynchronize(p->comp);
   release(p);
   delete p;
