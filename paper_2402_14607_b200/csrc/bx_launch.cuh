@@ -136,16 +136,51 @@ inline int sm_count() {
 // Shared memory per TMA CTA: two stages of both windows; kept small enough for
 // three resident CTAs per SM (228 KB) so tile loads of one CTA overlap the
 // integer work of the others.
-inline size_t tma_budget() {
-  static const size_t b = [] {
+// Shared-memory budget for one TMA stage pair: 72 KB, 96 KB for q >= 64
+// (paper q=80: 0.365 vs 0.372 ms; c4p q=58 unchanged at 72-96 KB and 10-18%
+// slower below 72 -- profiles/r02/tma_budget_sweep.txt).  BX_TMA_BUDGET_KB
+// overrides.
+inline size_t tma_budget(int q) {
+  static const int env = [] {
     const char* e = getenv("BX_TMA_BUDGET_KB");
-    return (size_t)(e ? atoi(e) : 72) * 1024;
+    return e ? atoi(e) : 0;
   }();
-  return b;
+  return (size_t)(env > 0 ? env : (q >= 64 ? 96 : 72)) * 1024;
 }
 
-// Occupancy of a TMA kernel configuration (setting its dynamic shared memory
-// limit first), memoised per (device, Q, threads, smem).
+// Raise a kernel's MaxDynamicSharedMemorySize to at least `smem` (per device).
+// The attribute is per function and shared by every launch configuration and
+// host thread, so it only ever grows: lowering it for a smaller tile would make
+// a concurrent or later launch of a larger tile fail with cudaErrorInvalidValue.
+inline cudaError_t raise_smem_limit(const void* k, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  struct Lim {
+    int dev;
+    const void* k;
+    size_t smem;
+  };
+  static std::mutex mu;
+  static std::vector<Lim> lims;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  for (Lim& l : lims)
+    if (l.dev == dev && l.k == k) {
+      if (l.smem >= smem) return cudaSuccess;
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) l.smem = smem;
+      return e;
+    }
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) lims.push_back(Lim{dev, k, smem});
+  return e;
+}
+
+// Occupancy of a TMA kernel configuration (raising its dynamic shared memory
+// limit first), memoised per (device, Q, threads, smem).  The kernel's limit
+// is a per-function attribute shared by every configuration of that Q, so it
+// only ever grows: lowering it for a smaller tile would make a later launch of
+// a memoised larger tile fail with cudaErrorInvalidValue.
 inline cudaError_t tma_occupancy(const void* k, int q, int threads, size_t smem, int* occ) {
   struct Entry {
     int dev, q, threads;
@@ -156,6 +191,8 @@ inline cudaError_t tma_occupancy(const void* k, int q, int threads, size_t smem,
   static std::vector<Entry> memo;
   int dev = 0;
   cudaGetDevice(&dev);
+  // every launch: the limit may not cover this smem yet on this device
+  if (cudaError_t e = raise_smem_limit(k, smem); e != cudaSuccess) return e;
   {
     std::lock_guard<std::mutex> g(mu);
     for (const Entry& e : memo)
@@ -163,10 +200,6 @@ inline cudaError_t tma_occupancy(const void* k, int q, int threads, size_t smem,
         *occ = e.occ;
         return cudaSuccess;
       }
-  }
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
   }
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, threads, smem);
   if (e != cudaSuccess) return e;
@@ -176,7 +209,7 @@ inline cudaError_t tma_occupancy(const void* k, int q, int threads, size_t smem,
 }
 
 inline void make_tma(LaunchCfg& c, int q, int n, int64_t nblocks) {
-  const size_t kTmaBudget = tma_budget();
+  const size_t kTmaBudget = tma_budget(q);
   const int64_t B = (int64_t)q * n;
   auto words = [&](int t) { return (int)((((((int64_t)t * B + 7) >> 3) + 4 + 32) + 15) / 16 * 4); };
   auto outw = [&](int t) { return (int)((31 + (int64_t)t * q + 31) >> 5) + 2; };
@@ -284,10 +317,8 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
   }
   if (c.staged) {
     auto k = eq_kernel<Q, true>;
-    if (c.smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-      if (e != cudaSuccess) return e;
-    }
+    if (cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(k), c.smem); e != cudaSuccess)
+      return e;
     k<<<(unsigned)c.grid, c.threads, c.smem, s>>>(a);
   } else {
     auto k = eq_kernel<Q, false>;

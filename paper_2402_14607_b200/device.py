@@ -45,7 +45,13 @@ def to_device_stream(data, device, pin: bool = False) -> tuple[torch.Tensor, int
     else:
         arr = np.frombuffer(memoryview(data), dtype=np.uint8) if not isinstance(data, np.ndarray) \
             else np.ascontiguousarray(data).reshape(-1).view(np.uint8)
-        src = torch.from_numpy(arr) if arr.size else torch.empty(0, dtype=torch.uint8)
+        if arr.size:
+            import warnings
+            with warnings.catch_warnings():   # read-only source buffers are only read
+                warnings.simplefilter("ignore")
+                src = torch.from_numpy(arr)
+        else:
+            src = torch.empty(0, dtype=torch.uint8)
         if pin and src.numel():
             src = src.pin_memory()
     n = src.numel()

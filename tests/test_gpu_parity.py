@@ -395,6 +395,23 @@ def test_native_pipe_random_push_sizes(depth):
         assert b"".join(out) == coracle.extract_eq(xb, yb, q, n, k), (q, n)
 
 
+def test_tma_tiles_of_one_width_interleaved():
+    """One kernel width launched with tiles of different shared-memory sizes
+    in turn (large, smaller, large again): the kernel's dynamic shared-memory
+    limit must never be lowered under a memoised larger configuration."""
+    rnd = random.Random(123)
+    for q in (72, 80, 99):
+        for n in (200, 61, 200, 33, 150, 200):
+            k = 40
+            nb = (k * q * n + 7) // 8 + 16
+            xb, yb = rnd.randbytes(nb), rnd.randbytes(nb)
+            xd, xn = D.to_device_stream(xb, "cuda")
+            yd, yn = D.to_device_stream(yb, "cuda")
+            got = D.extract_eq(xd, xn, yd, yn, q, n, k, x_bit0=3, y_bit0=3)
+            want = coracle.extract_eq(xb, yb, q, n, k, x_bit0=3, y_bit0=3)
+            assert got[:len(want)].cpu().numpy().tobytes() == want, (q, n)
+
+
 def test_native_pipe_async_latency_and_errors():
     """depth 2: a push returns the previous push's output; capacity and
     in-flight misuse are reported through bx_last_error."""
