@@ -899,6 +899,17 @@ __device__ __forceinline__ void ldg256(const uint4* p, uint4& a, uint4& b) {
                : "l"(p));
 }
 
+// Register double buffer of the next 256-bit unit pair in the q = 16 wide loop,
+// with the q = 16 kernel capped at 64 registers (4 CTAs/SM): c5 n=1024 3.37 vs
+// 3.41 ms; uncapped (81 registers, 3 CTAs) it is 5% slower, and the same
+// prefetch for q = 17..32 is 4% slower (profiles/r02/direct_prefetch_sweep.txt).
+#ifndef BX_PREFETCH_WIDE
+#define BX_PREFETCH_WIDE 1
+#endif
+#ifndef BX_PREFETCH_Q32
+#define BX_PREFETCH_Q32 0
+#endif
+
 // Unreduced inner product of one block's windows with 256-bit loads (units
 // even, xp / yp 32-byte aligned).
 template <int Q>
@@ -920,6 +931,24 @@ __device__ __forceinline__ Wide<cdiv(2 * Q - 1, 32)> direct_block_wide(const uin
   } else {
     Holes<Q> acc;
     acc.init();
+#if BX_PREFETCH_WIDE
+    // register double buffer: the next unit pair is in flight while this one
+    // multiplies (ncu: long_scoreboard was the top stall of the q = 16 loop)
+    uint4 X0, X1, Y0, Y1;
+    ldg256(xp, X0, X1);
+    ldg256(yp, Y0, Y1);
+#pragma unroll 1
+    for (int u = 0; u < units; u += 2) {
+      uint4 N0 = X0, N1 = X1, M0 = Y0, M1 = Y1;
+      if (u + 2 < units) {
+        ldg256(xp + u + 2, N0, N1);
+        ldg256(yp + u + 2, M0, M1);
+      }
+      direct_unit<Q>(X0, Y0, &acc);
+      direct_unit<Q>(X1, Y1, &acc);
+      X0 = N0; X1 = N1; Y0 = M0; Y1 = M1;
+    }
+#else
 #pragma unroll 1
     for (int u = 0; u < units; u += 2) {
       uint4 X0, X1, Y0, Y1;
@@ -928,6 +957,7 @@ __device__ __forceinline__ Wide<cdiv(2 * Q - 1, 32)> direct_block_wide(const uin
       direct_unit<Q>(X0, Y0, &acc);
       direct_unit<Q>(X1, Y1, &acc);
     }
+#endif
     c = acc.unreduced();
   }
   return c;
@@ -1013,6 +1043,9 @@ __device__ __forceinline__ Wide<8> direct_block_q128(const uint4* xp, const uint
 #ifndef BX_DIRECT_MINB_Q32
 #define BX_DIRECT_MINB_Q32 3
 #endif
+#ifndef BX_DIRECT_MINB_Q16
+#define BX_DIRECT_MINB_Q16 4
+#endif
 
 // q = 128 (three passes): 3 CTAs/SM (80 registers) for 8 or more units per
 // block (c3 n=8: +4% over one pass), 2 below (n=4: 3 CTAs cost 13%, 2 gain
@@ -1031,7 +1064,8 @@ template <int Q, int U>
 __global__ void __launch_bounds__(direct_threads(Q),
                                   (256 / direct_threads(Q)) *
                                       (Q == 128 ? BX_DIRECT_MINB_Q128(U)
-                                                : (Q > 32 ? 2 : (Q > 16 ? BX_DIRECT_MINB_Q32 : 1))))
+                                                : (Q > 32 ? 2 : (Q > 16 ? BX_DIRECT_MINB_Q32
+                                                                        : (Q > 8 ? BX_DIRECT_MINB_Q16 : 1)))))
     eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
@@ -1067,8 +1101,24 @@ __global__ void __launch_bounds__(direct_threads(Q),
 #pragma unroll 1
             for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
           } else {
+#if BX_PREFETCH_Q32
+            // register double buffer of one unit (q = 17..32)
+            uint4 X = __ldg(xp), Y = __ldg(yp);
+#pragma unroll 2
+            for (int u = 0; u < units; u++) {
+              uint4 NX = X, NY = Y;
+              if (u + 1 < units) {
+                NX = __ldg(xp + u + 1);
+                NY = __ldg(yp + u + 1);
+              }
+              direct_unit<Q>(X, Y, &acc);
+              X = NX;
+              Y = NY;
+            }
+#else
 #pragma unroll 2
             for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+#endif
           }
           c = acc.unreduced();
         }
