@@ -1046,6 +1046,9 @@ __device__ __forceinline__ Wide<8> direct_block_q128(const uint4* xp, const uint
 #ifndef BX_DIRECT_MINB_Q16
 #define BX_DIRECT_MINB_Q16 4
 #endif
+#ifndef BX_DIRECT_MINB_Q8
+#define BX_DIRECT_MINB_Q8 1
+#endif
 
 // q = 128 (three passes): 3 CTAs/SM (80 registers) for 8 or more units per
 // block (c3 n=8: +4% over one pass), 2 below (n=4: 3 CTAs cost 13%, 2 gain
@@ -1065,7 +1068,8 @@ __global__ void __launch_bounds__(direct_threads(Q),
                                   (256 / direct_threads(Q)) *
                                       (Q == 128 ? BX_DIRECT_MINB_Q128(U)
                                                 : (Q > 32 ? 2 : (Q > 16 ? BX_DIRECT_MINB_Q32
-                                                                        : (Q > 8 ? BX_DIRECT_MINB_Q16 : 1)))))
+                                                                        : (Q > 8 ? BX_DIRECT_MINB_Q16
+                                                                                 : (Q > 4 ? BX_DIRECT_MINB_Q8 : 1))))))
     eq_direct_kernel(const DirectArgs a) {
   constexpr int EW = cdiv(Q, 32);
   constexpr int CW = cdiv(2 * Q - 1, 32);
