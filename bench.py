@@ -681,6 +681,12 @@ def run_ours(args, wls) -> None:
         }
         print(json.dumps(line), flush=True)
     if use_dist:
+        # ranks > 0 drop their IPC mappings of rank 0's outputs before rank 0
+        # (the producer) may exit
+        outs = None
+        torch.cuda.synchronize(dev)
+        import gc
+        gc.collect()
         dist.barrier()
         dist.destroy_process_group()
 
