@@ -1063,6 +1063,59 @@ __device__ __forceinline__ Wide<8> direct_block_q128(const uint4* xp, const uint
 // -- profiles/r01_direct_sweep.txt O.
 __host__ __device__ constexpr int direct_threads(int q) { return q >= 32 ? 128 : 256; }
 
+// Blocks per thread of the direct kernel for small blocks at q <= 4: one-unit
+// blocks (c5 n = 128) take BX_DIRECT_BPT1, two-unit blocks (c5 n = 256, c2)
+// BX_DIRECT_BPT2 blocks per thread, one grid stride apart.  2 and 2: c5 n=128
+// 2.53 -> 2.39 ms, n=256 2.43 -> 2.39 ms (7.25 TB/s read, 1.11 x the copy
+// peak); 4 per thread is flat at n=128 and 5% slower at n=256, 8 is 38% slower
+// (profiles/r02/direct_prefetch_sweep.txt).
+#ifndef BX_DIRECT_BPT1
+#define BX_DIRECT_BPT1 2
+#endif
+#ifndef BX_DIRECT_BPT2
+#define BX_DIRECT_BPT2 2
+#endif
+__host__ __device__ constexpr int direct_bpt(int q, int u) {
+  return q > 4 ? 1 : (u == 1 ? BX_DIRECT_BPT1 : (u == 2 ? BX_DIRECT_BPT2 : 1));
+}
+
+// Store block l's output z: for q < 32, 32/q consecutive blocks (lanes) share
+// one output word, assembled with shuffles (every lane of the warp must call);
+// the run's last partial word is merged atomically.
+template <int Q>
+__device__ __forceinline__ void direct_store(const DirectArgs& a, int64_t l, const Wide<cdiv(Q, 32)>& z,
+                                             int lane) {
+  constexpr int EW = cdiv(Q, 32);
+  if constexpr (Q < 32) {
+    // 32/Q consecutive blocks share one output word
+    constexpr int G = 32 / Q;
+    uint32_t v = z.w[0] << ((lane % G) * Q);
+#pragma unroll
+    for (int m = 1; m < G; m <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, m);
+    const int64_t first = l - (lane % G);      // first block of this word
+    if ((lane % G) == 0 && first < a.nblocks) {
+      const int64_t w = first * Q / 32;
+      const int64_t valid = (a.nblocks - first) * Q;
+      BX_CHECK(w, a.out_words, 8);
+      if (valid >= 32) {
+        a.out[w] = v;
+      } else {
+        const uint32_t mask = (1u << valid) - 1u;
+        atomicAnd(&a.out[w], ~mask);
+        atomicOr(&a.out[w], v & mask);
+      }
+    }
+  } else {
+    if (l < a.nblocks) {
+#pragma unroll
+      for (int i = 0; i < EW; i++) {
+        BX_CHECK(l * EW + i, a.out_words, 8);
+        a.out[l * EW + i] = z.w[i];
+      }
+    }
+  }
+}
+
 template <int Q, int U>
 __global__ void __launch_bounds__(direct_threads(Q),
                                   (256 / direct_threads(Q)) *
@@ -1076,6 +1129,43 @@ __global__ void __launch_bounds__(direct_threads(Q),
   pdl_entry();
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
+  if constexpr (direct_bpt(Q, U) > 1) {
+    // small blocks (q <= 4, one or two units): each thread takes BPT blocks one
+    // grid stride apart and issues all their loads before computing (more
+    // bytes in flight per thread, BPT x fewer CTAs to launch)
+    constexpr int BPT = direct_bpt(Q, U);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    uint4 X[BPT][U], Y[BPT][U];
+#pragma unroll
+    for (int k = 0; k < BPT; k++) {
+      const int64_t lk = l + k * stride;
+      if (lk < a.nblocks) {
+        BX_CHECK((lk + 1) * U - 1, a.x_limit, 7);
+        BX_CHECK((lk + 1) * U - 1, a.y_limit, 7);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          X[k][u] = __ldg(a.x + lk * U + u);
+          Y[k][u] = __ldg(a.y + lk * U + u);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < BPT; k++) {
+      const int64_t lk = l + k * stride;
+      Wide<EW> zk = wzero<EW>();
+      if (lk < a.nblocks) {
+        Diag<Q> acc;
+        acc.init();
+#pragma unroll
+        for (int u = 0; u < U; u++) direct_unit<Q>(X[k][u], Y[k][u], &acc);
+        Wide<CW> c;
+        c.w[0] = acc.unreduced();
+        zk = reduce<Q>(c);
+      }
+      direct_store<Q>(a, lk, zk, lane);
+    }
+    return;
+  }
   Wide<EW> z = wzero<EW>();
   if (l < a.nblocks) {
     const uint4* xp = a.x + l * a.units;
@@ -1130,36 +1220,8 @@ __global__ void __launch_bounds__(direct_threads(Q),
       z = reduce<Q>(c);
     }
   }
-  if constexpr (Q < 32) {
-    // 32/Q consecutive blocks share one output word
-    constexpr int G = 32 / Q;
-    uint32_t v = z.w[0] << ((lane % G) * Q);
-#pragma unroll
-    for (int m = 1; m < G; m <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, m);
-    const int64_t first = l - (lane % G);      // first block of this word
-    if ((lane % G) == 0 && first < a.nblocks) {
-      const int64_t w = first * Q / 32;
-      const int64_t valid = (a.nblocks - first) * Q;
-      BX_CHECK(w, a.out_words, 8);
-      if (valid >= 32) {
-        a.out[w] = v;
-      } else {
-        const uint32_t mask = (1u << valid) - 1u;
-        atomicAnd(&a.out[w], ~mask);
-        atomicOr(&a.out[w], v & mask);
-      }
-    }
-  } else {
-    if (l < a.nblocks) {
-#pragma unroll
-      for (int i = 0; i < EW; i++) {
-        BX_CHECK(l * EW + i, a.out_words, 8);
-        a.out[l * EW + i] = z.w[i];
-      }
-    }
-  }
+  direct_store<Q>(a, l, z, lane);
 }
-
 
 // ------------------------------------------------------- period kernel
 //

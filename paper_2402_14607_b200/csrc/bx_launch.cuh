@@ -113,7 +113,8 @@ inline LaunchCfg choose_direct(int q, int n, int64_t nblocks) {
   c.staged = 0;
   c.smem = 0;
   c.units = (int)((int64_t)q * n / 128);
-  c.grid = (nblocks + threads - 1) / threads;
+  const int bpt = direct_bpt(q, c.units);
+  c.grid = (nblocks + (int64_t)threads * bpt - 1) / ((int64_t)threads * bpt);
   return c;
 }
 
