@@ -1075,8 +1075,12 @@ __host__ __device__ constexpr int direct_threads(int q) { return q >= 32 ? 128 :
 #ifndef BX_DIRECT_BPT2
 #define BX_DIRECT_BPT2 2
 #endif
+#ifndef BX_DIRECT_BPT8
+#define BX_DIRECT_BPT8 1
+#endif
 __host__ __device__ constexpr int direct_bpt(int q, int u) {
-  return q > 4 ? 1 : (u == 1 ? BX_DIRECT_BPT1 : (u == 2 ? BX_DIRECT_BPT2 : 1));
+  return q == 8 && u == 4 ? BX_DIRECT_BPT8
+                          : (q > 4 ? 1 : (u == 1 ? BX_DIRECT_BPT1 : (u == 2 ? BX_DIRECT_BPT2 : 1)));
 }
 
 // Store block l's output z: for q < 32, 32/q consecutive blocks (lanes) share
@@ -1129,7 +1133,7 @@ __global__ void __launch_bounds__(direct_threads(Q),
   pdl_entry();
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  if constexpr (direct_bpt(Q, U) > 1) {
+  if constexpr (Q <= 4 && direct_bpt(Q, U) > 1) {
     // small blocks (q <= 4, one or two units): each thread takes BPT blocks one
     // grid stride apart and issues all their loads before computing (more
     // bytes in flight per thread, BPT x fewer CTAs to launch)
@@ -1158,6 +1162,49 @@ __global__ void __launch_bounds__(direct_threads(Q),
         acc.init();
 #pragma unroll
         for (int u = 0; u < U; u++) direct_unit<Q>(X[k][u], Y[k][u], &acc);
+        Wide<CW> c;
+        c.w[0] = acc.unreduced();
+        zk = reduce<Q>(c);
+      }
+      direct_store<Q>(a, lk, zk, lane);
+    }
+    return;
+  }
+  if constexpr (Q == 8 && U == 4 && BX_DIRECT_BPT8 > 1) {
+    // q = 8, four units per block (c5 n = 512): the next block's 2 x 64 bytes
+    // are loaded (256-bit loads when aligned) while this block multiplies
+    constexpr int BPT = BX_DIRECT_BPT8;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    uint4 X[2][4], Y[2][4];
+    auto load = [&](int64_t lk, uint4 (&xs)[4], uint4 (&ys)[4]) {
+      const uint4* xp = a.x + lk * 4;
+      const uint4* yp = a.y + lk * 4;
+      if (a.wide) {
+        ldg256(xp, xs[0], xs[1]);
+        ldg256(xp + 2, xs[2], xs[3]);
+        ldg256(yp, ys[0], ys[1]);
+        ldg256(yp + 2, ys[2], ys[3]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          xs[u] = __ldg(xp + u);
+          ys[u] = __ldg(yp + u);
+        }
+      }
+    };
+    if (l < a.nblocks) load(l, X[0], Y[0]);
+#pragma unroll
+    for (int k = 0; k < BPT; k++) {
+      const int64_t lk = l + k * stride;
+      if (k + 1 < BPT && lk + stride < a.nblocks) load(lk + stride, X[(k + 1) & 1], Y[(k + 1) & 1]);
+      Wide<EW> zk = wzero<EW>();
+      if (lk < a.nblocks) {
+        BX_CHECK((lk + 1) * 4 - 1, a.x_limit, 7);
+        BX_CHECK((lk + 1) * 4 - 1, a.y_limit, 7);
+        Diag<Q> acc;
+        acc.init();
+#pragma unroll
+        for (int u = 0; u < 4; u++) direct_unit<Q>(X[k & 1][u], Y[k & 1][u], &acc);
         Wide<CW> c;
         c.w[0] = acc.unreduced();
         zk = reduce<Q>(c);
