@@ -167,15 +167,20 @@ def _device_inner_products(q: int, xs: Sequence[Sequence[int]], ys: Sequence[Seq
     groups: dict[int, list[int]] = {}
     for i, v in enumerate(xs):
         groups.setdefault(len(v), []).append(i)
+    from . import sharding
+
     for n, idx in groups.items():
         xb = _pack_vectors([xs[i] for i in idx], q)
         yb = _pack_vectors([ys[i] for i in idx], q)
-        xd, xn = D.to_device_stream(xb, dev)
-        yd, yn = D.to_device_stream(yb, dev)
-        res = D.extract_eq(xd, xn, yd, yn, q, n, len(idx))
-        nbytes = (len(idx) * q + 7) // 8
-        host = res[:nbytes].cpu().numpy().tobytes()
-        for i, v in zip(idx, _unpack_fields(host, len(idx), q)):
+        # one C call (staging, H2D, kernel, D2H) for the usual small batch
+        host = sharding.extract_small(xb, yb, q, n, len(idx), device=dev)
+        if host is None:
+            xd, xn = D.to_device_stream(xb, dev)
+            yd, yn = D.to_device_stream(yb, dev)
+            res = D.extract_eq(xd, xn, yd, yn, q, n, len(idx))
+            nbytes = (len(idx) * q + 7) // 8
+            host = res[:nbytes].cpu().numpy()
+        for i, v in zip(idx, _unpack_fields(host.tobytes(), len(idx), q)):
             out[i] = v
     return out
 

@@ -82,10 +82,13 @@ def test_launch_info_geometry():
             assert li["direct"] == (q in (1, 2, 4, 8, 16, 32, 64, 128, 24, 40, 48, 56)
                                     and q * n % 128 == 0)
             ntiles = -(-10_000 // li["tile"])
+            # small direct blocks (q <= 4, one or two 128-bit units) take two
+            # blocks per thread (bx_core.cuh direct_bpt)
+            bpt = 2 if li["direct"] and q <= 4 and q * n // 128 in (1, 2) else 1
             if li["tma"]:
                 assert 0 < li["grid"] <= ntiles and li["staged"]
             else:
-                assert li["grid"] == ntiles
+                assert li["grid"] == -(-ntiles // bpt)
 
 
 def test_golden_plans_and_bounds(golden):

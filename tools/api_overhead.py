@@ -58,6 +58,14 @@ def main():
         np.frombuffer(xq, np.uint8).ctypes.data, len(xq), 0, np.frombuffer(yq, np.uint8).ctypes.data,
         len(yq), 0, q, n, k // 8, oa.ctypes.data, 0))
     res["extract_packed"] = med(lambda: sharding.extract_packed(x1, y1, q, n, k))
+    f32, f128 = bx.field(32), bx.field(128)
+    res["gf_mul_q32"] = med(lambda: f32.mul(0x12345678, 0x9ABCDEF1), 200)
+    res["gf_mul_q128"] = med(lambda: f128.mul((1 << 127) | 12345, (1 << 100) | 777), 200)
+    res["gf_inv_q128"] = med(lambda: f128.inv((1 << 127) | 12345), 100)
+    xs = [list(range(1, 72))] * 64
+    f80 = bx.field(80)
+    pairs = [bx.BlockPair(i + 1, f80, tuple(v), tuple(reversed(v))) for i, v in enumerate(xs)]
+    res["run_parallel_64_blocks_q80_n71"] = med(lambda: list(bx.run_parallel(iter(pairs), 1)), 50)
     res["api_run"] = med(lambda: bx.extract_eq(x1, y1, plan).run(io.BytesIO()))
     print(json.dumps(res))
 
