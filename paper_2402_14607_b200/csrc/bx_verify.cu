@@ -15,6 +15,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "bx_core.cuh"
+
 namespace bx {
 
 struct SmallField {
@@ -167,50 +169,93 @@ __global__ void gf_ip_generic_kernel(int q, const uint32_t* modulus, const uint3
   }
 }
 
-// c = a * b mod (x^q + m) for q-bit a, b (4-word operands)
-__device__ __forceinline__ void mulmod128(int q, const uint32_t (&m)[4], const uint32_t (&a)[4],
-                                          const uint32_t (&b)[4], uint32_t (&r)[4]) {
-  uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int i = 0; i < q; i++)
-    if ((a[i >> 5] >> (i & 31)) & 1u) shl_xor8(c, b, i);
-  for (int i = 2 * q - 2; i >= q; i--) {
-    if ((c[i >> 5] >> (i & 31)) & 1u) {
-      c[i >> 5] ^= 1u << (i & 31);
-      shl_xor8(c, m, i - q);
+// Fold table of a runtime modulus: R[i] = x^(q+i) mod P for i in [0, q)
+// (reference gf2q.py:124-133), 4 words per entry, built once per CTA.
+__device__ void fold_table128(int q, const uint32_t (&m)[4], uint32_t (*R)[4]) {
+  uint32_t t[4] = {m[0], m[1], m[2], m[3]};   // x^q mod P = P - x^q
+  for (int i = 0; i < q; i++) {
+#pragma unroll
+    for (int w = 0; w < 4; w++) R[i][w] = t[w];
+    // t <<= 1; if bit q set: t ^= x^q + m (clears bit q, adds the low part)
+    const uint32_t top = (t[(q - 1) >> 5] >> ((q - 1) & 31)) & 1u;
+    t[3] = (t[3] << 1) | (t[2] >> 31);
+    t[2] = (t[2] << 1) | (t[1] >> 31);
+    t[1] = (t[1] << 1) | (t[0] >> 31);
+    t[0] <<= 1;
+    if (q < 128) t[q >> 5] &= ~(1u << (q & 31));
+    if (top) {
+#pragma unroll
+      for (int w = 0; w < 4; w++) t[w] ^= m[w];
     }
   }
+}
+
+// r = a * b mod P for q-bit a, b: the 255-bit carry-less product with the
+// holes kernel (Holes<128>: Karatsuba over 16-bit halves, IMAD products),
+// then the high part folded with R.  All register-resident; the bit scan of
+// the high part is unrolled over static word/bit positions.
+__device__ __forceinline__ void mulmod128(int q, const uint32_t (*R)[4], const uint32_t (&a)[4],
+                                          const uint32_t (&b)[4], uint32_t (&r)[4]) {
+  Holes<128> h;
+  h.init();
+  h.add(a, b);
+  const Wide<8> c = h.unreduced();
+  uint32_t z[4];
 #pragma unroll
   for (int w = 0; w < 4; w++) {
     const int lo = 32 * w;
-    uint32_t val = c[w];
+    uint32_t val = c.w[w];
     if (lo >= q) val = 0;
     else if (q - lo < 32) val &= (1u << (q - lo)) - 1u;
-    r[w] = val;
+    z[w] = val;
   }
+#pragma unroll
+  for (int w = 0; w < 8; w++) {
+    uint32_t word = c.w[w];
+    // bits of this word at positions >= q
+    const int lo = 32 * w;
+    if (lo + 31 < q) continue;
+    if (lo < q) word &= ~((q - lo) >= 32 ? 0xFFFFFFFFu : ((1u << (q - lo)) - 1u));
+    while (word) {
+      const int bit = __ffs(word) - 1;
+      word &= word - 1u;
+      const uint32_t* f = R[lo + bit - q];
+#pragma unroll
+      for (int k = 0; k < 4; k++) z[k] ^= f[k];
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < 4; w++) r[w] = z[w];
 }
 
 // out[v] = x[v]^e[v] by square-and-multiply over the exponent's bits, LSB
 // first (the reference GFContext.pow loop, gf2q.py:171-182), one thread per
 // element; 128-bit little-endian operands.
-__global__ void gf_pow_kernel(int q, const uint32_t* modulus, const uint32_t* x, const uint32_t* e,
-                              int64_t count, uint32_t* out) {
+__global__ void __launch_bounds__(128) gf_pow_kernel(int q, const uint32_t* modulus,
+                                                     const uint32_t* x, const uint32_t* e,
+                                                     int64_t count, uint32_t* out) {
+  __shared__ uint32_t R[128][4];
+  const uint32_t m[4] = {modulus[0], modulus[1], modulus[2], modulus[3]};
+  if (threadIdx.x == 0) fold_table128(q, m, R);
+  __syncthreads();
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= count) return;
-  const uint32_t m[4] = {modulus[0], modulus[1], modulus[2], modulus[3]};
   uint32_t b[4] = {x[v * 4], x[v * 4 + 1], x[v * 4 + 2], x[v * 4 + 3]};
   uint32_t r[4] = {1u, 0u, 0u, 0u};
+  const uint32_t ew[4] = {e[v * 4], e[v * 4 + 1], e[v * 4 + 2], e[v * 4 + 3]};
   int top = -1;
-  for (int i = 127; i >= 0 && top < 0; i--)
-    if ((e[v * 4 + (i >> 5)] >> (i & 31)) & 1u) top = i;
+#pragma unroll
+  for (int w = 3; w >= 0; w--)
+    if (top < 0 && ew[w]) top = 32 * w + 31 - __clz(ew[w]);
   for (int i = 0; i <= top; i++) {
     uint32_t t[4];
-    if ((e[v * 4 + (i >> 5)] >> (i & 31)) & 1u) {
-      mulmod128(q, m, r, b, t);
+    if ((ew[i >> 5] >> (i & 31)) & 1u) {
+      mulmod128(q, R, r, b, t);
 #pragma unroll
       for (int w = 0; w < 4; w++) r[w] = t[w];
     }
     if (i < top) {
-      mulmod128(q, m, b, b, t);
+      mulmod128(q, R, b, b, t);
 #pragma unroll
       for (int w = 0; w < 4; w++) b[w] = t[w];
     }
