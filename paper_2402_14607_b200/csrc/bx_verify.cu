@@ -124,50 +124,12 @@ cudaError_t launch_rows_uniform(const uint32_t* counts, uint32_t nrows, uint32_t
 }  // namespace bx
 
 // ---------------------------------------------------------------------------
-// Runtime-modulus inner products (GFContext with a caller-chosen irreducible
-// modulus; reference gf2q.py:99-183 allows any).  Not a hot path: one thread
-// per vector, shift-and-XOR carry-less products over 4-word (128-bit)
-// operands accumulated unreduced, one bit-serial reduction by the modulus.
+// Runtime-modulus field arithmetic (GFContext with a caller-chosen irreducible
+// modulus, reference gf2q.py:99-189 allows any; and pow / inv for every
+// modulus).  Not the extraction path: one thread per vector or element,
+// 128-bit operands, carry-less products with the holes kernel (Holes<128>),
+// reduction through a per-CTA fold table of the modulus.
 namespace bx {
-
-__device__ __forceinline__ void shl_xor8(uint32_t (&c)[8], const uint32_t (&b)[4], int s) {
-  const int ws = s >> 5, bs = s & 31;
-#pragma unroll
-  for (int i = 0; i < 4; i++) {
-    const uint32_t v = b[i];
-    if (ws + i < 8) c[ws + i] ^= v << bs;
-    if (bs && ws + i + 1 < 8) c[ws + i + 1] ^= v >> (32 - bs);
-  }
-}
-
-__global__ void gf_ip_generic_kernel(int q, const uint32_t* modulus, const uint32_t* x,
-                                     const uint32_t* y, int n, int64_t nvec, uint32_t* out) {
-  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nvec) return;
-  uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int j = 0; j < n; j++) {
-    const uint32_t* a = x + (v * n + j) * 4;
-    uint32_t b[4] = {y[(v * n + j) * 4], y[(v * n + j) * 4 + 1], y[(v * n + j) * 4 + 2],
-                     y[(v * n + j) * 4 + 3]};
-    for (int i = 0; i < q; i++)
-      if ((a[i >> 5] >> (i & 31)) & 1u) shl_xor8(c, b, i);
-  }
-  // reduce: for every set bit i >= q (top down) XOR modulus << (i - q)
-  uint32_t m[4] = {modulus[0], modulus[1], modulus[2], modulus[3]};  // full modulus minus x^q
-  for (int i = 2 * q - 2; i >= q; i--) {
-    if ((c[i >> 5] >> (i & 31)) & 1u) {
-      c[i >> 5] ^= 1u << (i & 31);
-      shl_xor8(c, m, i - q);
-    }
-  }
-  for (int w = 0; w < 4; w++) {
-    const int lo = 32 * w;
-    uint32_t val = c[w];
-    if (lo >= q) val = 0;
-    else if (q - lo < 32) val &= (1u << (q - lo)) - 1u;
-    out[v * 4 + w] = val;
-  }
-}
 
 // Fold table of a runtime modulus: R[i] = x^(q+i) mod P for i in [0, q)
 // (reference gf2q.py:124-133), 4 words per entry, built once per CTA.
@@ -190,6 +152,9 @@ __device__ void fold_table128(int q, const uint32_t (&m)[4], uint32_t (*R)[4]) {
   }
 }
 
+__device__ __forceinline__ void reduce_runtime(int q, const uint32_t (*R)[4], const Wide<8>& c,
+                                               uint32_t (&r)[4]);
+
 // r = a * b mod P for q-bit a, b: the 255-bit carry-less product with the
 // holes kernel (Holes<128>: Karatsuba over 16-bit halves, IMAD products),
 // then the high part folded with R.  All register-resident; the bit scan of
@@ -199,7 +164,12 @@ __device__ __forceinline__ void mulmod128(int q, const uint32_t (*R)[4], const u
   Holes<128> h;
   h.init();
   h.add(a, b);
-  const Wide<8> c = h.unreduced();
+  reduce_runtime(q, R, h.unreduced(), r);
+}
+
+// z = c mod P (runtime modulus through the fold table R)
+__device__ __forceinline__ void reduce_runtime(int q, const uint32_t (*R)[4], const Wide<8>& c,
+                                               uint32_t (&r)[4]) {
   uint32_t z[4];
 #pragma unroll
   for (int w = 0; w < 4; w++) {
@@ -226,6 +196,33 @@ __device__ __forceinline__ void mulmod128(int q, const uint32_t (*R)[4], const u
   }
 #pragma unroll
   for (int w = 0; w < 4; w++) r[w] = z[w];
+}
+
+// Inner products under a runtime modulus (GFContext(q, modulus).mul / ext_ip,
+// reference gf2q.py:99-169): the unreduced products of a vector are summed
+// with the holes kernel (Holes<128>) and reduced once with the CTA's fold
+// table of the modulus.
+__global__ void __launch_bounds__(128) gf_ip_generic_kernel(int q, const uint32_t* modulus,
+                                                            const uint32_t* x, const uint32_t* y,
+                                                            int n, int64_t nvec, uint32_t* out) {
+  __shared__ uint32_t R[128][4];
+  const uint32_t m[4] = {modulus[0], modulus[1], modulus[2], modulus[3]};
+  if (threadIdx.x == 0) fold_table128(q, m, R);
+  __syncthreads();
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvec) return;
+  Holes<128> h;
+  h.init();
+  for (int j = 0; j < n; j++) {
+    const uint4 a = reinterpret_cast<const uint4*>(x)[v * n + j];
+    const uint4 b = reinterpret_cast<const uint4*>(y)[v * n + j];
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+    h.add(aw, bw);
+  }
+  uint32_t z[4];
+  reduce_runtime(q, R, h.unreduced(), z);
+#pragma unroll
+  for (int w = 0; w < 4; w++) out[v * 4 + w] = z[w];
 }
 
 // out[v] = x[v]^e[v] by square-and-multiply over the exponent's bits, LSB
