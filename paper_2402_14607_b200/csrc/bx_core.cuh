@@ -310,6 +310,30 @@ __device__ __forceinline__ Parts split_lo(uint32_t w) {  // low half of w
   return Parts{{w & 0x9249u, w & 0x2492u, w & 0x4924u}};
 }
 
+#ifndef BX_SPLIT_IMAD
+#define BX_SPLIT_IMAD 0
+#endif
+#if BX_SPLIT_IMAD
+// -1 from the constant bank: ptxas cannot fold it, so h - p0 - p1 stays two
+// IMADs on the FMA pipe instead of becoming an IADD3 on the ALU pipe
+__constant__ uint32_t kMinusOne = 0xFFFFFFFFu;
+#endif
+
+// A 16-bit half with no bits above bit 15 (e.g. w >> 16): the third residue
+// class is h - p0 - p1 (disjoint bits, no borrows), moved to the FMA pipe
+// when BX_SPLIT_IMAD is set.
+__device__ __forceinline__ Parts split_clean(uint32_t h) {
+#if BX_SPLIT_IMAD
+  const uint32_t p0 = h & 0x9249u, p1 = h & 0x2492u;
+  uint32_t p2;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(p2) : "r"(p1), "r"(kMinusOne), "r"(h));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(p2) : "r"(p0), "r"(kMinusOne), "r"(p2));
+  return Parts{{p0, p1, p2}};
+#else
+  return Parts{{h & 0x9249u, h & 0x2492u, h & 0x4924u}};
+#endif
+}
+
 __device__ __forceinline__ Parts pxor(const Parts& a, const Parts& b) {
   return Parts{{a.p[0] ^ b.p[0], a.p[1] ^ b.p[1], a.p[2] ^ b.p[2]}};
 }
@@ -450,6 +474,12 @@ struct Holes {
     split_halves<NH>(xw, xo);
     split_halves<NH>(yw, yo);
     kara_acc<NH, 0, K>(xo, yo, acc);
+  }
+
+  // one 16-bit element per operand, both with no bits above bit 15
+  __device__ __forceinline__ void add_clean(uint32_t x, uint32_t y) {
+    static_assert(NH == 1, "add_clean is for q <= 16");
+    holes16(split_clean(x), split_clean(y), acc[0]);
   }
 
   __device__ __forceinline__ void add2(const uint32_t (&xa)[EW], const uint32_t (&ya)[EW],
@@ -857,7 +887,7 @@ __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void
         acc.add2(a0, b0, a1, b1);
 #else
         acc.add(a0, b0);
-        acc.add(a1, b1);
+        acc.add_clean(a1[0], b1[0]);   // high halves: no bits above 15 after the shift
 #endif
       }
     } else if constexpr (4 / EW >= 2 && Holes<Q>::kPair && BX_DIRECT_PAIR) {
