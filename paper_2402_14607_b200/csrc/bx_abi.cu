@@ -95,17 +95,32 @@ struct DeviceScope {
   bool reaches(const void* p) const {
     const int d = device_of(p);
     if (d < 0 || d == dev) return true;
-    static int memo[64][64];   // 0 unknown, 1 yes, 2 no
+    static std::atomic<int> memo[64][64];   // 0 unknown, 1 yes, 2 no
     if (dev >= 64 || d >= 64) return true;
-    if (!memo[dev][d]) {
+    int m = memo[dev][d].load(std::memory_order_acquire);
+    if (!m) {
       int ok = 0;
       if (cudaDeviceCanAccessPeer(&ok, dev, d) != cudaSuccess) {
         cudaGetLastError();
         ok = 0;
       }
-      memo[dev][d] = ok ? 1 : 2;
+      if (ok) {
+        // Capability is not access: a buffer another process exported over
+        // CUDA IPC is mapped in ITS device's context here (torch opens the
+        // handle under that device), so `dev` -- current for this scope --
+        // must enable peer access to d itself.  The setting belongs to the
+        // primary contexts, shared with the caller's runtime; "already
+        // enabled" (by torch or NCCL) is success.
+        const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          if (e != cudaErrorPeerAccessAlreadyEnabled) ok = 0;
+        }
+      }
+      m = ok ? 1 : 2;
+      memo[dev][d].store(m, std::memory_order_release);
     }
-    return memo[dev][d] == 1;
+    return m == 1;
   }
   DeviceScope(const DeviceScope&) = delete;
   DeviceScope& operator=(const DeviceScope&) = delete;

@@ -66,6 +66,12 @@ inline LaunchCfg choose_launch(int q, int n, int64_t nblocks) {
   c.family = q <= kDiagMaxQ ? 0 : 1;
   const int64_t B = (int64_t)q * n;
   int64_t units, target;
+  // elements (word chunks for the diag family) a thread should own before a
+  // block is split over another thread: BX_TPB_TARGET overrides (A/B runs)
+  static const int env_target = [] {
+    const char* e = getenv("BX_TPB_TARGET");
+    return e ? atoi(e) : 0;
+  }();
   if (c.family == 0) {
     units = cdiv(n, 32 / q);
     target = 8;
@@ -73,6 +79,7 @@ inline LaunchCfg choose_launch(int q, int n, int64_t nblocks) {
     units = n;
     target = 8;   // amortise the per-thread Karatsuba recombination
   }
+  if (env_target > 0) target = env_target;
   int tpb = 1;
   while (tpb < 32 && units / (2 * tpb) >= target) tpb *= 2;
   c.tpb_log2 = 0;
