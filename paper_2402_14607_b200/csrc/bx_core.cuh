@@ -40,6 +40,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "bx_moduli.h"
@@ -503,6 +504,188 @@ struct Holes {
   }
 };
 
+// ------------------------------------------ dot-product holes (IDP.2A, q >= 9)
+//
+// The same residue-class trick with sm_100a's full-rate 16x8 two-term dot
+// product (dp2a -> IDP.2A, 64/clk/SM on the FMA pipe like IMAD, co-issues with
+// LOP3: tools/microbench/idp.cu): a = [h1 : h0] holds the same 16-bit half of
+// TWO consecutive elements, b = bytes [h1.b1, h0.b1, h1.b0, h0.b0] of the other
+// operand's halves, and
+//     dp2a.lo(a & MX_r, b & MY_s) = h0_r (x) h0.b0_s + h1_r (x) h1.b0_s
+// (dp2a.hi the same with the high bytes).  A holed 16-bit half has <= 6 bits,
+// a holed byte <= 3, so a coefficient counts <= 3 products per term and <= 6
+// per instruction: still no carry into the next same-residue position.  One
+// LOP3 now masks two halves (or four bytes) at once, and the high halves need
+// no shift (one PRMT packs two elements): 11 instead of 20 ALU operations per
+// q = 32 element pair in front of the same 27 FMA-pipe products, 3.5 instead
+// of 7 at q = 16.  The high-byte products are accumulated apart and shifted by
+// 8 once per block.
+#ifndef BX_DP2A
+#define BX_DP2A 1
+#endif
+
+__device__ __forceinline__ Parts dsplit_x(uint32_t w) {   // two 16-bit halves
+  return Parts{{w & 0x92499249u, w & 0x24922492u, w & 0x49244924u}};
+}
+__device__ __forceinline__ Parts dsplit_y(uint32_t w) {   // four bytes, in-byte residues
+  return Parts{{w & 0x49494949u, w & 0x92929292u, w & 0x24242424u}};
+}
+
+struct DotAcc {
+  uint32_t lo[3], hi[3];
+};
+
+// one packed pair (two elements' halves): 18 IDP.2A into 6 accumulators
+__device__ __forceinline__ void dot16(const Parts& x, const Parts& y, DotAcc& A) {
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    uint32_t l = 0u, h = 0u;
+#pragma unroll
+    for (int r = 0; r < 3; r++) {
+      const int s = (c + 3 - r) % 3;
+      l ^= __dp2a_lo(x.p[r], y.p[s], 0u);
+      h ^= __dp2a_hi(x.p[r], y.p[s], 0u);
+    }
+    A.lo[c] ^= l;
+    A.hi[c] ^= h;
+  }
+}
+
+// two packed pairs (four elements): 6 products + the accumulator = three
+// 3-input LOP3 per accumulator instead of four
+__device__ __forceinline__ void dot16x2(const Parts& xa, const Parts& ya, const Parts& xb,
+                                        const Parts& yb, DotAcc& A) {
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    uint32_t l = 0u, h = 0u;
+#pragma unroll
+    for (int r = 0; r < 3; r++) {
+      const int s = (c + 3 - r) % 3;
+      l ^= __dp2a_lo(xa.p[r], ya.p[s], 0u) ^ __dp2a_lo(xb.p[r], yb.p[s], 0u);
+      h ^= __dp2a_hi(xa.p[r], ya.p[s], 0u) ^ __dp2a_hi(xb.p[r], yb.p[s], 0u);
+    }
+    A.lo[c] ^= l;
+    A.hi[c] ^= h;
+  }
+}
+
+template <int M, int L0, int K>
+__device__ __forceinline__ void dkara_acc(const Parts* xo, const Parts* yo, DotAcc (&acc)[K]) {
+  if constexpr (M == 1) {
+    dot16(xo[0], yo[0], acc[L0]);
+  } else {
+    constexpr int h = (M + 1) / 2;
+    dkara_acc<h, L0, K>(xo, yo, acc);
+    dkara_acc<M - h, L0 + kara_leaves(h), K>(xo + h, yo + h, acc);
+    Parts xm[h], ym[h];
+#pragma unroll
+    for (int i = 0; i < h; i++) {
+      xm[i] = (i + h < M) ? pxor(xo[i], xo[i + h]) : xo[i];
+      ym[i] = (i + h < M) ? pxor(yo[i], yo[i + h]) : yo[i];
+    }
+    dkara_acc<h, L0 + kara_leaves(h) + kara_leaves(M - h), K>(xm, ym, acc);
+  }
+}
+
+template <int M, int L0, int K>
+__device__ __forceinline__ void dkara_acc2(const Parts* xa, const Parts* ya, const Parts* xb,
+                                           const Parts* yb, DotAcc (&acc)[K]) {
+  if constexpr (M == 1) {
+    dot16x2(xa[0], ya[0], xb[0], yb[0], acc[L0]);
+  } else {
+    constexpr int h = (M + 1) / 2;
+    dkara_acc2<h, L0, K>(xa, ya, xb, yb, acc);
+    dkara_acc2<M - h, L0 + kara_leaves(h), K>(xa + h, ya + h, xb + h, yb + h, acc);
+    Parts xam[h], yam[h], xbm[h], ybm[h];
+#pragma unroll
+    for (int i = 0; i < h; i++) {
+      xam[i] = (i + h < M) ? pxor(xa[i], xa[i + h]) : xa[i];
+      yam[i] = (i + h < M) ? pxor(ya[i], ya[i + h]) : ya[i];
+      xbm[i] = (i + h < M) ? pxor(xb[i], xb[i + h]) : xb[i];
+      ybm[i] = (i + h < M) ? pxor(yb[i], yb[i + h]) : yb[i];
+    }
+    dkara_acc2<h, L0 + kara_leaves(h) + kara_leaves(M - h), K>(xam, yam, xbm, ybm, acc);
+  }
+}
+
+template <int Q>
+struct Dot {
+  static constexpr int EW = cdiv(Q, 32);
+  static constexpr int NH = cdiv(Q, 16);
+  static constexpr int K = kara_leaves(NH);
+  static constexpr int CW = cdiv(2 * Q - 1, 32);
+  DotAcc acc[K];
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int s = 0; s < K; s++)
+#pragma unroll
+      for (int c = 0; c < 3; c++) acc[s].lo[c] = acc[s].hi[c] = 0u;
+  }
+
+  // Residue parts of two elements a, b packed half by half: x side
+  // [b.half_u : a.half_u], y side [b.half_u.b1, a.half_u.b1, b.half_u.b0, a.half_u.b0].
+  static __device__ __forceinline__ void pack_x(const uint32_t (&a)[EW], const uint32_t (&b)[EW],
+                                                Parts (&o)[NH]) {
+#pragma unroll
+    for (int u = 0; u < NH; u++)
+      o[u] = dsplit_x(__byte_perm(a[u >> 1], b[u >> 1], (u & 1) ? 0x7632u : 0x5410u));
+  }
+  static __device__ __forceinline__ void pack_y(const uint32_t (&a)[EW], const uint32_t (&b)[EW],
+                                                Parts (&o)[NH]) {
+#pragma unroll
+    for (int u = 0; u < NH; u++)
+      o[u] = dsplit_y(__byte_perm(a[u >> 1], b[u >> 1], (u & 1) ? 0x7362u : 0x5140u));
+  }
+
+  // two elements
+  __device__ __forceinline__ void add2(const uint32_t (&xa)[EW], const uint32_t (&ya)[EW],
+                                       const uint32_t (&xb)[EW], const uint32_t (&yb)[EW]) {
+    Parts px[NH], py[NH];
+    pack_x(xa, xb, px);
+    pack_y(ya, yb, py);
+    dkara_acc<NH, 0, K>(px, py, acc);
+  }
+
+  // four elements
+  __device__ __forceinline__ void add4(const uint32_t (&xa)[EW], const uint32_t (&ya)[EW],
+                                       const uint32_t (&xb)[EW], const uint32_t (&yb)[EW],
+                                       const uint32_t (&xc)[EW], const uint32_t (&yc)[EW],
+                                       const uint32_t (&xd)[EW], const uint32_t (&yd)[EW]) {
+    Parts px0[NH], py0[NH], px1[NH], py1[NH];
+    pack_x(xa, xb, px0);
+    pack_y(ya, yb, py0);
+    pack_x(xc, xd, px1);
+    pack_y(yc, yd, py1);
+    dkara_acc2<NH, 0, K>(px0, py0, px1, py1, acc);
+  }
+
+  // q = 16: a stream word already holds two elements' (only) halves
+  __device__ __forceinline__ void add_words2(uint32_t x0, uint32_t y0, uint32_t x1, uint32_t y1) {
+    static_assert(NH == 1, "add_words2 is for q = 16");
+    dot16x2(dsplit_x(x0), dsplit_y(__byte_perm(y0, 0u, 0x3120u)), dsplit_x(x1),
+            dsplit_y(__byte_perm(y1, 0u, 0x3120u)), acc[0]);
+  }
+
+  __device__ __forceinline__ Wide<CW> unreduced() const {
+    uint32_t P[K];
+#pragma unroll
+    for (int s = 0; s < K; s++) {
+      const uint32_t l = (acc[s].lo[0] & 0x49249249u) | (acc[s].lo[1] & 0x92492492u) |
+                         (acc[s].lo[2] & 0x24924924u);
+      const uint32_t h = (acc[s].hi[0] & 0x49249249u) | (acc[s].hi[1] & 0x92492492u) |
+                         (acc[s].hi[2] & 0x24924924u);
+      P[s] = l ^ (h << 8);
+    }
+    Wide<CW> c = wzero<CW>();
+    kara_fin<NH, 0, 1u, K, CW>(P, c);
+    return c;
+  }
+};
+
+// accumulator of the direct kernels' holes widths
+__host__ __device__ constexpr bool dot_direct_q(int q) { return BX_DP2A && (q == 16 || q == 32); }
+
 // ----------------------------------------------------------------- kernel
 
 struct EqArgs {
@@ -866,6 +1049,9 @@ struct DirectArgs {
 #endif
 
 template <int Q>
+using DirectHoles = typename std::conditional<dot_direct_q(Q), Dot<Q>, Holes<Q>>::type;
+
+template <int Q>
 __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void* accp) {
   if constexpr (Q <= kDiagMaxQ) {
     Diag<Q>& acc = *static_cast<Diag<Q>*>(accp);
@@ -873,6 +1059,16 @@ __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void
     acc.add(X.y, Y.y);
     acc.add(X.z, Y.z);
     acc.add(X.w, Y.w);
+  } else if constexpr (dot_direct_q(Q)) {
+    Dot<Q>& acc = *static_cast<Dot<Q>*>(accp);
+    if constexpr (Q == 16) {
+      acc.add_words2(X.x, Y.x, X.y, Y.y);
+      acc.add_words2(X.z, Y.z, X.w, Y.w);
+    } else {
+      const uint32_t xa[1] = {X.x}, xb[1] = {X.y}, xc[1] = {X.z}, xd[1] = {X.w};
+      const uint32_t ya[1] = {Y.x}, yb[1] = {Y.y}, yc[1] = {Y.z}, yd[1] = {Y.w};
+      acc.add4(xa, ya, xb, yb, xc, yc, xd, yd);
+    }
   } else {
     Holes<Q>& acc = *static_cast<Holes<Q>*>(accp);
     constexpr int EW = cdiv(Q, 32);
@@ -959,7 +1155,7 @@ __device__ __forceinline__ Wide<cdiv(2 * Q - 1, 32)> direct_block_wide(const uin
     }
     c.w[0] = acc.unreduced();
   } else {
-    Holes<Q> acc;
+    DirectHoles<Q> acc;
     acc.init();
 #if BX_PREFETCH_WIDE
     // register double buffer: the next unit pair is in flight while this one
@@ -1252,7 +1448,7 @@ __global__ void __launch_bounds__(direct_threads(Q),
     // U > 0: the unit count is a compile-time constant (fully unrolled,
     // all loads issued up front); U == 0: runtime count.
     const int units = U > 0 ? U : a.units;
-    if (Q <= 16 && a.wide) {
+    if ((Q <= 16 || Q == 32) && a.wide) {
       z = reduce<Q>(direct_block_wide<Q>(xp, yp, units));
     } else {
       Wide<CW> c;
@@ -1266,7 +1462,7 @@ __global__ void __launch_bounds__(direct_threads(Q),
         if constexpr (Q == 128 && BX_Q128_PASSES) {
           c = direct_block_q128(xp, yp, units, a.wide);
         } else {
-          Holes<Q> acc;
+          DirectHoles<Q> acc;
           acc.init();
           if constexpr (Q > 32) {
 #pragma unroll 1

@@ -49,6 +49,18 @@ inline bool direct_ok(int q, int n, int64_t x_bit0, int64_t y_bit0, int64_t out_
          out_bit0 % 32 == 0 && (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
 }
 
+// 256-bit loads in the q = 32 direct kernel (BX_WIDE32=0/1 for A/B runs)
+#ifndef BX_WIDE32_DEFAULT
+#define BX_WIDE32_DEFAULT 0
+#endif
+inline bool wide32_enabled() {
+  static const int v = [] {
+    const char* e = getenv("BX_WIDE32");
+    return e ? atoi(e) : BX_WIDE32_DEFAULT;
+  }();
+  return v != 0;
+}
+
 // 256-bit loads in the q = 16 and q = 128 direct kernels (BX_WIDE=0 disables, for A/B runs).
 inline bool wide_loads_enabled() {
   static const bool on = [] {
@@ -280,7 +292,8 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
       // 256-bit loads (two units per load; sweeps C, P, T): q = 8, 16, 128 at
       // any even unit count; q <= 4 from 8 units per block up (the fully
       // unrolled 128-bit form of those is register-bound: q=4 n=256 +57%)
-      d.wide = ((Q == 8 || Q == 16 || Q == 128 || (Q <= 4 && c.units >= 8)) && c.units % 2 == 0 &&
+      d.wide = ((Q == 8 || Q == 16 || Q == 128 || (Q == 32 && wide32_enabled()) ||
+                 (Q <= 4 && c.units >= 8)) && c.units % 2 == 0 &&
                 wide_loads_enabled() &&
                 ((reinterpret_cast<uintptr_t>(d.x) | reinterpret_cast<uintptr_t>(d.y)) & 31) == 0)
                    ? 1 : 0;
