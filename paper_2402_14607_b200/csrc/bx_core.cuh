@@ -523,6 +523,18 @@ struct Holes {
 #ifndef BX_DP2A
 #define BX_DP2A 1
 #endif
+// the tile / period kernels (any q >= 9) with the dot-product form
+#ifndef BX_DP2A_TILE
+#define BX_DP2A_TILE 1
+#endif
+// widest element (16-bit halves) the tile / period kernels take in the dot form:
+// its K(NH) x 6 accumulators must fit the kernels' register caps
+#ifndef BX_DOT_TILE_MAX_HALVES
+#define BX_DOT_TILE_MAX_HALVES 4
+#endif
+#ifndef BX_DOT_QUAD_MAX_HALVES
+#define BX_DOT_QUAD_MAX_HALVES 8
+#endif
 
 __device__ __forceinline__ Parts dsplit_x(uint32_t w) {   // two 16-bit halves
   return Parts{{w & 0x92499249u, w & 0x24922492u, w & 0x49244924u}};
@@ -638,6 +650,19 @@ struct Dot {
       o[u] = dsplit_y(__byte_perm(a[u >> 1], b[u >> 1], (u & 1) ? 0x7362u : 0x5140u));
   }
 
+  static constexpr bool kPair = true;
+  // four elements per accumulate step (three 3-input LOP3 per accumulator and
+  // four elements instead of two per two) while the operand parts fit
+  static constexpr bool kQuad = NH <= BX_DOT_QUAD_MAX_HALVES;
+
+  // a single element (tails): its partner is zero
+  __device__ __forceinline__ void add(const uint32_t (&xa)[EW], const uint32_t (&ya)[EW]) {
+    uint32_t z[EW];
+#pragma unroll
+    for (int i = 0; i < EW; i++) z[i] = 0u;
+    add2(xa, ya, z, z);
+  }
+
   // two elements
   __device__ __forceinline__ void add2(const uint32_t (&xa)[EW], const uint32_t (&ya)[EW],
                                        const uint32_t (&xb)[EW], const uint32_t (&yb)[EW]) {
@@ -685,6 +710,14 @@ struct Dot {
 
 // accumulator of the direct kernels' holes widths
 __host__ __device__ constexpr bool dot_direct_q(int q) { return BX_DP2A && (q == 16 || q == 32); }
+// accumulator of the tile and period kernels
+template <int Q>
+using TileHoles = typename std::conditional<(BX_DP2A_TILE != 0 && cdiv(Q, 16) <= BX_DOT_TILE_MAX_HALVES),
+                                            Dot<Q>, Holes<Q>>::type;
+template <typename H>
+struct has_quad { static constexpr bool value = false; };
+template <int Q>
+struct has_quad<Dot<Q>> { static constexpr bool value = Dot<Q>::kQuad; };
 
 // ----------------------------------------------------------------- kernel
 
@@ -755,10 +788,22 @@ __device__ __forceinline__ void tile_compute(const EqArgs& a, const uint32_t* sx
       }
       c.w[0] = acc.unreduced();
     } else {
-      Holes<Q> acc;
+      using H = TileHoles<Q>;
+      H acc;
       acc.init();
       int j = sub;
-      for (; Holes<Q>::kPair && j + tpb < a.n; j += 2 * tpb) {
+      if constexpr (has_quad<H>::value) {
+        for (; j + 3 * tpb < a.n; j += 4 * tpb) {
+          uint32_t xw[4][EW], yw[4][EW];
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            read_elem<Q>(sx, xo + (T)(j + k * tpb) * (T)Q, xlim, xw[k]);
+            read_elem<Q>(sy, yo + (T)(j + k * tpb) * (T)Q, ylim, yw[k]);
+          }
+          acc.add4(xw[0], yw[0], xw[1], yw[1], xw[2], yw[2], xw[3], yw[3]);
+        }
+      }
+      for (; H::kPair && j + tpb < a.n; j += 2 * tpb) {
         uint32_t xw[EW], yw[EW], xw2[EW], yw2[EW];
         read_elem<Q>(sx, xo + (T)j * (T)Q, xlim, xw);
         read_elem<Q>(sy, yo + (T)j * (T)Q, ylim, yw);
@@ -946,8 +991,16 @@ __device__ __forceinline__ void pdl_entry() {
 #endif
 }
 
+// Resident CTAs the TMA kernel's registers are capped for at 32 < q <= 64: the
+// dot form keeps 6 accumulators per leaf (36 / 54 for 3 / 4 halves), which
+// spills under the 85-register cap of three CTAs (c4p 2.66 ms) and runs in
+// 128 registers with two (c4p 2.19 ms; the IMAD form with three: 2.38 ms --
+// profiles/r02/dp2a_sweep.txt).
+#ifndef BX_TMA_MINB_Q64
+#define BX_TMA_MINB_Q64 2
+#endif
 template <int Q>
-__global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? 3 : 2))) eq_tma_kernel(const EqArgs a) {
+__global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? BX_TMA_MINB_Q64 : 2))) eq_tma_kernel(const EqArgs a) {
   pdl_entry();
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ __align__(8) uint64_t bars[2];
@@ -1541,7 +1594,8 @@ __global__ void __launch_bounds__(BX_PERIOD_THREADS, BX_PERIOD_MINB) eq_period_k
     const uint4* yp = a.y + l * a.units;
     BX_CHECK((l + 1) * a.units - 1, a.x_limit, 7);
     BX_CHECK((l + 1) * a.units - 1, a.y_limit, 7);
-    Holes<Q> acc;
+    using H = TileHoles<Q>;
+    H acc;
     acc.init();
     const int periods = a.units / UNITS;
 #pragma unroll 1
@@ -1553,30 +1607,42 @@ __global__ void __launch_bounds__(BX_PERIOD_THREADS, BX_PERIOD_MINB) eq_period_k
         xw[4 * u] = X.x; xw[4 * u + 1] = X.y; xw[4 * u + 2] = X.z; xw[4 * u + 3] = X.w;
         yw[4 * u] = Y.x; yw[4 * u + 1] = Y.y; yw[4 * u + 2] = Y.z; yw[4 * u + 3] = Y.w;
       }
-#pragma unroll
-      for (int e = 0; e < ELEMS; e += 2) {
-        uint32_t xa[EW], ya[EW], xb[EW], yb[EW];
+      // element e of the period: compile-time funnel shifts
+      auto elem = [&](int e, uint32_t (&xe)[EW], uint32_t (&ye)[EW]) {
 #pragma unroll
         for (int i = 0; i < EW; i++) {
-          const int oa = e * Q + 32 * i, ob = (e + 1) * Q + 32 * i;
-          const int wa = oa >> 5, sa = oa & 31, wb = ob >> 5, sb = ob & 31;
-          const uint32_t xa1 = wa + 1 < WORDS ? xw[wa + 1] : 0u, ya1 = wa + 1 < WORDS ? yw[wa + 1] : 0u;
-          const uint32_t xb1 = wb + 1 < WORDS ? xw[wb + 1] : 0u, yb1 = wb + 1 < WORDS ? yw[wb + 1] : 0u;
-          xa[i] = sa ? __funnelshift_r(xw[wa], xa1, sa) : xw[wa];
-          ya[i] = sa ? __funnelshift_r(yw[wa], ya1, sa) : yw[wa];
-          xb[i] = sb ? __funnelshift_r(xw[wb], xb1, sb) : xw[wb];
-          yb[i] = sb ? __funnelshift_r(yw[wb], yb1, sb) : yw[wb];
+          const int o = e * Q + 32 * i;
+          const int w = o >> 5, sh = o & 31;
+          const uint32_t x1 = w + 1 < WORDS ? xw[w + 1] : 0u, y1 = w + 1 < WORDS ? yw[w + 1] : 0u;
+          xe[i] = sh ? __funnelshift_r(xw[w], x1, sh) : xw[w];
+          ye[i] = sh ? __funnelshift_r(yw[w], y1, sh) : yw[w];
         }
         if constexpr (Q % 32) {
           constexpr uint32_t m = (1u << (Q % 32)) - 1u;
-          xa[EW - 1] &= m; ya[EW - 1] &= m; xb[EW - 1] &= m; yb[EW - 1] &= m;
+          xe[EW - 1] &= m; ye[EW - 1] &= m;
         }
+      };
+      if constexpr (has_quad<H>::value && ELEMS % 4 == 0) {
+#pragma unroll
+        for (int e = 0; e < ELEMS; e += 4) {
+          uint32_t xe[4][EW], ye[4][EW];
+#pragma unroll
+          for (int k = 0; k < 4; k++) elem(e + k, xe[k], ye[k]);
+          acc.add4(xe[0], ye[0], xe[1], ye[1], xe[2], ye[2], xe[3], ye[3]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < ELEMS; e += 2) {
+          uint32_t xa[EW], ya[EW], xb[EW], yb[EW];
+          elem(e, xa, ya);
+          elem(e + 1, xb, yb);
 #if BX_PERIOD_PAIR
-        acc.add2(xa, ya, xb, yb);
+          acc.add2(xa, ya, xb, yb);
 #else
-        acc.add(xa, ya);
-        acc.add(xb, yb);
+          acc.add(xa, ya);
+          acc.add(xb, yb);
 #endif
+        }
       }
     }
     z = reduce<Q>(acc.unreduced());
