@@ -1172,8 +1172,35 @@ __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void
 // warp read windows q*n/8 bytes apart, so every load touches 32 lines; at
 // q = 16 the 128-bit-load kernel is L1-throughput bound and the 256-bit loads
 // halve its L1 requests (+8%, profiles/r01_direct_sweep.txt).
+#ifndef BX_L2_HINT
+#define BX_L2_HINT 0
+#endif
+#if BX_L2_HINT == 256
+#define BX_LD_HINT ".L2::256B"
+#elif BX_L2_HINT == 128
+#define BX_LD_HINT ".L2::128B"
+#elif BX_L2_HINT == 64
+#define BX_LD_HINT ".L2::64B"
+#else
+#define BX_LD_HINT ""
+#endif
+
+// 128-bit read-only load of a stream unit (with the L2 sector-promotion hint
+// BX_L2_HINT when set)
+__device__ __forceinline__ uint4 ldg128(const uint4* p) {
+#if BX_L2_HINT
+  uint4 a;
+  asm volatile("ld.global.nc" BX_LD_HINT ".v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
+               : "l"(p));
+  return a;
+#else
+  return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ void ldg256(const uint4* p, uint4& a, uint4& b) {
-  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  asm volatile("ld.global.nc" BX_LD_HINT ".v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
                : "l"(p));
 }
@@ -1283,10 +1310,10 @@ __device__ __forceinline__ void q128_pass(const uint4* xp, const uint4* yp, int 
       ldg256(xp + u, X0, X1);
       ldg256(yp + u, Y0, Y1);
     } else {
-      X0 = __ldg(xp + u);
-      Y0 = __ldg(yp + u);
-      X1 = __ldg(xp + u + 1);
-      Y1 = __ldg(yp + u + 1);
+      X0 = ldg128(xp + u);
+      Y0 = ldg128(yp + u);
+      X1 = ldg128(xp + u + 1);
+      Y1 = ldg128(yp + u + 1);
     }
     uint32_t a[2], b[2], a2[2], b2[2];
     q128_part<P>(X0, a);
@@ -1297,8 +1324,8 @@ __device__ __forceinline__ void q128_pass(const uint4* xp, const uint4* yp, int 
   }
   if (u < units) {
     uint32_t a[2], b[2];
-    q128_part<P>(__ldg(xp + u), a);
-    q128_part<P>(__ldg(yp + u), b);
+    q128_part<P>(ldg128(xp + u), a);
+    q128_part<P>(ldg128(yp + u), b);
     acc.add(a, b);
   }
   const Wide<4> p = acc.unreduced();
@@ -1319,6 +1346,10 @@ __device__ __forceinline__ Wide<8> direct_block_q128(const uint4* xp, const uint
   return c;
 }
 
+#ifndef BX_Q32_UNROLL
+#define BX_Q32_UNROLL 2
+#endif
+constexpr int kQ32Unroll = BX_Q32_UNROLL;
 #ifndef BX_DIRECT_MINB_Q32
 #define BX_DIRECT_MINB_Q32 3
 #endif
@@ -1427,8 +1458,8 @@ __global__ void __launch_bounds__(direct_threads(Q),
         BX_CHECK((lk + 1) * U - 1, a.y_limit, 7);
 #pragma unroll
         for (int u = 0; u < U; u++) {
-          X[k][u] = __ldg(a.x + lk * U + u);
-          Y[k][u] = __ldg(a.y + lk * U + u);
+          X[k][u] = ldg128(a.x + lk * U + u);
+          Y[k][u] = ldg128(a.y + lk * U + u);
         }
       }
     }
@@ -1466,8 +1497,8 @@ __global__ void __launch_bounds__(direct_threads(Q),
       } else {
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-          xs[u] = __ldg(xp + u);
-          ys[u] = __ldg(yp + u);
+          xs[u] = ldg128(xp + u);
+          ys[u] = ldg128(yp + u);
         }
       }
     };
@@ -1509,7 +1540,7 @@ __global__ void __launch_bounds__(direct_threads(Q),
         Diag<Q> acc;
         acc.init();
 #pragma unroll 4
-        for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+        for (int u = 0; u < units; u++) direct_unit<Q>(ldg128(xp + u), ldg128(yp + u), &acc);
         c.w[0] = acc.unreduced();
       } else {
         if constexpr (Q == 128 && BX_Q128_PASSES) {
@@ -1519,25 +1550,25 @@ __global__ void __launch_bounds__(direct_threads(Q),
           acc.init();
           if constexpr (Q > 32) {
 #pragma unroll 1
-            for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+            for (int u = 0; u < units; u++) direct_unit<Q>(ldg128(xp + u), ldg128(yp + u), &acc);
           } else {
 #if BX_PREFETCH_Q32
             // register double buffer of one unit (q = 17..32)
-            uint4 X = __ldg(xp), Y = __ldg(yp);
+            uint4 X = ldg128(xp), Y = ldg128(yp);
 #pragma unroll 2
             for (int u = 0; u < units; u++) {
               uint4 NX = X, NY = Y;
               if (u + 1 < units) {
-                NX = __ldg(xp + u + 1);
-                NY = __ldg(yp + u + 1);
+                NX = ldg128(xp + u + 1);
+                NY = ldg128(yp + u + 1);
               }
               direct_unit<Q>(X, Y, &acc);
               X = NX;
               Y = NY;
             }
 #else
-#pragma unroll 2
-            for (int u = 0; u < units; u++) direct_unit<Q>(__ldg(xp + u), __ldg(yp + u), &acc);
+#pragma unroll kQ32Unroll
+            for (int u = 0; u < units; u++) direct_unit<Q>(ldg128(xp + u), ldg128(yp + u), &acc);
 #endif
           }
           c = acc.unreduced();
@@ -1603,7 +1634,7 @@ __global__ void __launch_bounds__(BX_PERIOD_THREADS, BX_PERIOD_MINB) eq_period_k
       uint32_t xw[WORDS], yw[WORDS];
 #pragma unroll
       for (int u = 0; u < UNITS; u++) {
-        const uint4 X = __ldg(xp + p * UNITS + u), Y = __ldg(yp + p * UNITS + u);
+        const uint4 X = ldg128(xp + p * UNITS + u), Y = ldg128(yp + p * UNITS + u);
         xw[4 * u] = X.x; xw[4 * u + 1] = X.y; xw[4 * u + 2] = X.z; xw[4 * u + 3] = X.w;
         yw[4 * u] = Y.x; yw[4 * u + 1] = Y.y; yw[4 * u + 2] = Y.z; yw[4 * u + 3] = Y.w;
       }
