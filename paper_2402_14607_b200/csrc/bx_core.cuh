@@ -1604,6 +1604,14 @@ __host__ __device__ constexpr bool period_q(int q) {
 #define BX_PERIOD_PAIR 1
 #endif
 
+#ifndef BX_PERIOD_QUADLOOP
+#define BX_PERIOD_QUADLOOP 1
+#endif
+#ifndef BX_PERIOD_QUAD_UNROLL
+#define BX_PERIOD_QUAD_UNROLL 1
+#endif
+constexpr int kPeriodQuadUnroll = BX_PERIOD_QUAD_UNROLL;
+
 #ifndef BX_PERIOD_THREADS
 #define BX_PERIOD_THREADS 128
 #endif
@@ -1628,6 +1636,47 @@ __global__ void __launch_bounds__(BX_PERIOD_THREADS, BX_PERIOD_MINB) eq_period_k
     using H = TileHoles<Q>;
     H acc;
     acc.init();
+    if constexpr (BX_PERIOD_QUADLOOP && has_quad<H>::value && Q == 56) {
+      // Four elements are Q/8 whole words and the shift pattern repeats with
+      // them, so the loop runs over quads with 32-bit loads: a body of one quad
+      // (650 instructions at q = 56) instead of a whole period (2,562, which
+      // missed the instruction cache: ncu no_instruction 0.57 warps per issue).
+      // c2p 0.270 -> 0.261 ms; at q = 24 / 40 / 48 the 32-bit loads make the
+      // kernel L1-wavefront bound (-35% / -6% / -60%), so only q = 56 takes it
+      // (profiles/r02/dp2a_sweep.txt, sweep 8).
+      constexpr int WP = Q / 8;
+      const uint32_t* xq = reinterpret_cast<const uint32_t*>(xp);
+      const uint32_t* yq = reinterpret_cast<const uint32_t*>(yp);
+      const int quads = a.units * 32 / Q;
+#pragma unroll kPeriodQuadUnroll
+      for (int k = 0; k < quads; k++) {
+        uint32_t xw[WP], yw[WP];
+#pragma unroll
+        for (int i = 0; i < WP; i++) {
+          xw[i] = __ldg(xq + k * WP + i);
+          yw[i] = __ldg(yq + k * WP + i);
+        }
+        uint32_t xe[4][EW], ye[4][EW];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+#pragma unroll
+          for (int i = 0; i < EW; i++) {
+            const int o = e * Q + 32 * i;
+            const int w = o >> 5, sh = o & 31;
+            const uint32_t x1 = w + 1 < WP ? xw[w + 1 < WP ? w + 1 : 0] : 0u;
+            const uint32_t y1 = w + 1 < WP ? yw[w + 1 < WP ? w + 1 : 0] : 0u;
+            xe[e][i] = sh ? __funnelshift_r(xw[w], x1, sh) : xw[w];
+            ye[e][i] = sh ? __funnelshift_r(yw[w], y1, sh) : yw[w];
+          }
+          if constexpr (Q % 32) {
+            constexpr uint32_t m = (1u << (Q % 32)) - 1u;
+            xe[e][EW - 1] &= m; ye[e][EW - 1] &= m;
+          }
+        }
+        acc.add4(xe[0], ye[0], xe[1], ye[1], xe[2], ye[2], xe[3], ye[3]);
+      }
+      z = reduce<Q>(acc.unreduced());
+    } else {
     const int periods = a.units / UNITS;
 #pragma unroll 1
     for (int p = 0; p < periods; p++) {
@@ -1677,6 +1726,7 @@ __global__ void __launch_bounds__(BX_PERIOD_THREADS, BX_PERIOD_MINB) eq_period_k
       }
     }
     z = reduce<Q>(acc.unreduced());
+    }
   }
   // the warp's 32 blocks own output words [first*Q/32, first*Q/32 + Q)
   uint32_t* so = sout[warp];
