@@ -1283,6 +1283,12 @@ __device__ __forceinline__ Wide<cdiv(2 * Q - 1, 32)> direct_block_wide(const uin
 #define BX_Q128_PASSES 1
 #endif
 
+// q = 128 passes with the dot-product accumulator (0: IMAD holes, 1: pairs,
+// 2: four elements per step)
+#ifndef BX_Q128_DOT
+#define BX_Q128_DOT 0
+#endif
+
 template <int P>
 __device__ __forceinline__ void q128_part(const uint4& v, uint32_t (&o)[2]) {
   if constexpr (P == 0) {
@@ -1300,9 +1306,34 @@ __device__ __forceinline__ void q128_part(const uint4& v, uint32_t (&o)[2]) {
 template <int P>
 __device__ __forceinline__ void q128_pass(const uint4* xp, const uint4* yp, int units, bool wide,
                                           Wide<8>& c) {
-  Holes<64> acc;
+  typename std::conditional<(BX_Q128_DOT != 0), Dot<64>, Holes<64>>::type acc;
   acc.init();
   int u = 0;
+#if BX_Q128_DOT == 2
+#pragma unroll 1
+  for (; u + 3 < units; u += 4) {     // four elements per accumulate step
+    uint4 X[4], Y[4];
+    if (wide) {
+      ldg256(xp + u, X[0], X[1]);
+      ldg256(yp + u, Y[0], Y[1]);
+      ldg256(xp + u + 2, X[2], X[3]);
+      ldg256(yp + u + 2, Y[2], Y[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        X[k] = ldg128(xp + u + k);
+        Y[k] = ldg128(yp + u + k);
+      }
+    }
+    uint32_t a[4][2], b[4][2];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      q128_part<P>(X[k], a[k]);
+      q128_part<P>(Y[k], b[k]);
+    }
+    acc.add4(a[0], b[0], a[1], b[1], a[2], b[2], a[3], b[3]);
+  }
+#endif
 #pragma unroll 1
   for (; u + 1 < units; u += 2) {
     uint4 X0, X1, Y0, Y1;
