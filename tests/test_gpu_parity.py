@@ -80,8 +80,9 @@ def test_every_q_random_shapes_and_offsets():
 
 
 def test_extremes_all_ones_and_zeros():
-    for q in (1, 2, 4, 7, 8, 9, 16, 31, 32, 33, 63, 64, 65, 100, 127, 128):
-        for n in (1, 5, 64, 257):
+    # 24, 40, 48, 56: the period kernel; 58, 80: the planner / paper TMA shapes
+    for q in (1, 2, 4, 7, 8, 9, 16, 24, 31, 32, 33, 40, 48, 56, 58, 63, 64, 65, 80, 100, 127, 128):
+        for n in (1, 5, 48, 64, 257):
             k = 40
             nb = (k * q * n + 7) // 8
             for fill in (b"\xff", b"\x00", b"\x55"):
