@@ -618,6 +618,46 @@ def run_ours(args, wls) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    # ---- informational (N = 1, several legs): the same sweep with the two host
+    # streams uploaded ONCE per step and every leg run on the device-resident
+    # copies through the public API (`e2e` above re-uploads them for every leg)
+    once = None
+    if world == 1 and len(wls) > 1 and e2e_err is None and args.e2e_steps > 0:
+        try:
+            torch.cuda.synchronize(dev)
+            xu = D.empty_stream(xn, dev)
+            yu = D.empty_stream(yn, dev)
+            s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+            def once_pass():
+                t0 = time.perf_counter()
+                with torch.cuda.stream(s1):
+                    xu[:xn].copy_(xh[:xn], non_blocking=True)
+                with torch.cuda.stream(s2):
+                    yu[:yn].copy_(yh[:yn], non_blocking=True)
+                s1.synchronize()
+                s2.synchronize()
+                t1 = time.perf_counter()
+                res = []
+                for wl in wls:
+                    snk = KeepSink()
+                    bx.extract_eq(xu[:xn], yu[:yn], wl.plan(), device=dev).run(snk)
+                    res.append(snk.data)
+                return res, time.perf_counter() - t0, t1 - t0
+
+            if args.e2e_warmup:
+                once_pass()
+            res1, once_s, once_h2d_s = once_pass()
+            once = {"value": sum(job_bits) / once_s / 1e9, "unit": UNIT, "seconds_per_step": once_s,
+                    "h2d_seconds": once_h2d_s, "h2d_bytes_per_step": xn + yn, "d2h_bytes_per_step": d2h,
+                    "bit_exact_vs_device_run": all(bytes(r) == o[:ob].cpu().numpy().tobytes()
+                                                   for r, o, ob in zip(res1, outs, obytes)),
+                    "path": "x, y pinned host tensors copied to the device once per step (two copy "
+                            "streams), then extract_eq(device tensors, plan).run(sink) for every leg"}
+            del xu, yu, res1
+        except Exception as exc:  # noqa: BLE001 - informational only
+            once = {"error": repr(exc)}
+
     _trace(rank, "cpu")
     # ---- CPU baselines (rank 0, N = 1 only)
     cpu = None
@@ -670,6 +710,7 @@ def run_ours(args, wls) -> None:
                              "paper_2402_14607_b200.extract_eq(pinned host tensors, plan).run(sink) "
                              "per leg: H2D of both streams, kernels, D2H of the packed output"),
                     "bit_exact_vs_device_run": e2e_ok},
+            **({"e2e_upload_once": once} if once is not None else {}),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": sampler.summary(),
