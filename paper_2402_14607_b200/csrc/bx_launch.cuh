@@ -89,7 +89,11 @@ inline LaunchCfg choose_launch(int q, int n, int64_t nblocks) {
     target = 8;
   } else {
     units = n;
-    target = 8;   // amortise the per-thread Karatsuba recombination
+    // amortise the per-thread Karatsuba recombination; the dot form accumulates
+    // four elements per step and recombines twice the accumulators, so it
+    // wants 16 (c4p 2.20 -> 2.05 ms, q=37 n=50 -13%, q=20 n=60 -16%; the IMAD
+    // form at q = 80 is 2% slower with 16 -- profiles/r02/dp2a_sweep.txt, sweep 10)
+    target = (BX_DP2A_TILE != 0 && cdiv(q, 16) <= BX_DOT_TILE_MAX_HALVES) ? 16 : 8;
   }
   if (env_target > 0) target = env_target;
   int tpb = 1;
