@@ -1638,6 +1638,9 @@ __host__ __device__ constexpr bool period_q(int q) {
 #ifndef BX_PERIOD_QUADLOOP
 #define BX_PERIOD_QUADLOOP 1
 #endif
+#ifndef BX_PERIOD_QUAD_PREFETCH
+#define BX_PERIOD_QUAD_PREFETCH 0
+#endif
 #ifndef BX_PERIOD_QUAD_UNROLL
 #define BX_PERIOD_QUAD_UNROLL 1
 #endif
@@ -1679,14 +1682,39 @@ __global__ void __launch_bounds__(BX_PERIOD_THREADS, BX_PERIOD_MINB) eq_period_k
       const uint32_t* xq = reinterpret_cast<const uint32_t*>(xp);
       const uint32_t* yq = reinterpret_cast<const uint32_t*>(yp);
       const int quads = a.units * 32 / Q;
+#if BX_PERIOD_QUAD_PREFETCH
+      uint32_t nx[WP], ny[WP];
+#pragma unroll
+      for (int i = 0; i < WP; i++) {
+        nx[i] = __ldg(xq + i);
+        ny[i] = __ldg(yq + i);
+      }
+#endif
 #pragma unroll kPeriodQuadUnroll
       for (int k = 0; k < quads; k++) {
         uint32_t xw[WP], yw[WP];
+#if BX_PERIOD_QUAD_PREFETCH
+        // register double buffer: the next quad's words are in flight while
+        // this one multiplies
+#pragma unroll
+        for (int i = 0; i < WP; i++) {
+          xw[i] = nx[i];
+          yw[i] = ny[i];
+        }
+        if (k + 1 < quads) {
+#pragma unroll
+          for (int i = 0; i < WP; i++) {
+            nx[i] = __ldg(xq + (k + 1) * WP + i);
+            ny[i] = __ldg(yq + (k + 1) * WP + i);
+          }
+        }
+#else
 #pragma unroll
         for (int i = 0; i < WP; i++) {
           xw[i] = __ldg(xq + k * WP + i);
           yw[i] = __ldg(yq + k * WP + i);
         }
+#endif
         uint32_t xe[4][EW], ye[4][EW];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
