@@ -999,8 +999,11 @@ __device__ __forceinline__ void pdl_entry() {
 #ifndef BX_TMA_MINB_Q64
 #define BX_TMA_MINB_Q64 2
 #endif
+#ifndef BX_TMA_MINB_Q128
+#define BX_TMA_MINB_Q128 2
+#endif
 template <int Q>
-__global__ void __launch_bounds__(256, (Q > 64 ? 2 : (Q > 32 ? BX_TMA_MINB_Q64 : 2))) eq_tma_kernel(const EqArgs a) {
+__global__ void __launch_bounds__(256, (Q > 64 ? BX_TMA_MINB_Q128 : (Q > 32 ? BX_TMA_MINB_Q64 : 2))) eq_tma_kernel(const EqArgs a) {
   pdl_entry();
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ __align__(8) uint64_t bars[2];
