@@ -11,7 +11,7 @@
 // gf2q.py:156-169) because reduction mod P is GF(2)-linear; the carry-less
 // products are therefore accumulated UNREDUCED over the block and reduced once.
 //
-// There is no carry-less multiply instruction on the GPU.  Two integer-pipe
+// There is no carry-less multiply instruction on the GPU.  Three integer-pipe
 // formulations are used, chosen at compile time by Q:
 //
 //  * Diag (Q <= 8): a 32-bit chunk holds E = 32/Q elements.  For every shift
@@ -34,6 +34,12 @@
 //    whole block and recombined and masked once per block.
 //    IMAD.WIDE is avoided: it issues at 1/3 the rate of IMAD on sm_100a
 //    (profiles/r01_pipes_microbench.txt).
+//
+//  * Dot (Q >= 9, up to four halves; the q = 16 / 32 direct kernels, the tile
+//    and period kernels up to q = 64): the same holes with IDP.2A, a two-term
+//    16x8 dot product at IMAD's rate -- two elements' halves per operand, one
+//    LOP3 masking two halves or four bytes (see "dot-product holes" below).
+//    Same product count, about a quarter fewer ALU operations.
 //
 // Reduction mod P uses the shipped sparse modulus (bx_moduli.h) with all shift
 // amounts compile-time constants.
