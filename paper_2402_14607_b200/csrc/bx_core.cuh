@@ -715,7 +715,14 @@ struct Dot {
 };
 
 // accumulator of the direct kernels' holes widths
-__host__ __device__ constexpr bool dot_direct_q(int q) { return BX_DP2A && (q == 16 || q == 32); }
+// the q = 64 direct kernel in the dot form (four elements per step): q=64 n=50
+// 0.367 -> 0.311 ms, n=64 / n=8 -9% (profiles/r02/dp2a_sweep.txt, sweep 16)
+#ifndef BX_DP2A_Q64
+#define BX_DP2A_Q64 1
+#endif
+__host__ __device__ constexpr bool dot_direct_q(int q) {
+  return BX_DP2A && (q == 16 || q == 32 || (q == 64 && BX_DP2A_Q64));
+}
 // accumulator of the tile and period kernels
 template <int Q>
 using TileHoles = typename std::conditional<(BX_DP2A_TILE != 0 && cdiv(Q, 16) <= BX_DOT_TILE_MAX_HALVES),
@@ -1126,6 +1133,10 @@ __device__ __forceinline__ void direct_unit(const uint4& X, const uint4& Y, void
     if constexpr (Q == 16) {
       acc.add_words2(X.x, Y.x, X.y, Y.y);
       acc.add_words2(X.z, Y.z, X.w, Y.w);
+    } else if constexpr (Q == 64) {     // one unit = two elements
+      const uint32_t xa[2] = {X.x, X.y}, xb[2] = {X.z, X.w};
+      const uint32_t ya[2] = {Y.x, Y.y}, yb[2] = {Y.z, Y.w};
+      acc.add2(xa, ya, xb, yb);
     } else {
       const uint32_t xa[1] = {X.x}, xb[1] = {X.y}, xc[1] = {X.z}, xd[1] = {X.w};
       const uint32_t ya[1] = {Y.x}, yb[1] = {Y.y}, yc[1] = {Y.z}, yd[1] = {Y.w};
@@ -1588,7 +1599,20 @@ __global__ void __launch_bounds__(direct_threads(Q),
         } else {
           DirectHoles<Q> acc;
           acc.init();
-          if constexpr (Q > 32) {
+          if constexpr (Q == 64 && dot_direct_q(Q)) {
+            int u = 0;
+#pragma unroll 1
+            for (; u + 1 < units; u += 2) {     // four elements per accumulate step
+              const uint4 X0 = ldg128(xp + u), Y0 = ldg128(yp + u);
+              const uint4 X1 = ldg128(xp + u + 1), Y1 = ldg128(yp + u + 1);
+              const uint32_t xa[2] = {X0.x, X0.y}, xb[2] = {X0.z, X0.w};
+              const uint32_t xc[2] = {X1.x, X1.y}, xd[2] = {X1.z, X1.w};
+              const uint32_t ya[2] = {Y0.x, Y0.y}, yb[2] = {Y0.z, Y0.w};
+              const uint32_t yc[2] = {Y1.x, Y1.y}, yd[2] = {Y1.z, Y1.w};
+              acc.add4(xa, ya, xb, yb, xc, yc, xd, yd);
+            }
+            if (u < units) direct_unit<Q>(ldg128(xp + u), ldg128(yp + u), &acc);
+          } else if constexpr (Q > 32) {
 #pragma unroll 1
             for (int u = 0; u < units; u++) direct_unit<Q>(ldg128(xp + u), ldg128(yp + u), &acc);
           } else {
