@@ -217,6 +217,7 @@ int bx_extract_eq(const void* x, int64_t x_bytes, int64_t x_bit0, const void* y,
   a.tpb_log2 = c.tpb_log2;
   a.tile_blocks = c.tile;
   a.stage_words = c.stage_words;
+  a.stages = c.stages;
   // ABI guarantee: readable through round_up(bytes, 16) + 16
   a.x_limit = ((x_bytes + 15) / 16) * 4 + 4;
   a.y_limit = ((y_bytes + 15) / 16) * 4 + 4;

@@ -748,6 +748,7 @@ struct EqArgs {
   int tpb_log2;        // threads per block = 1 << tpb_log2 (<= 32)
   int tile_blocks;     // blocks per CTA
   int stage_words;     // smem words per source (STAGED only)
+  int stages;          // TMA kernel: input stages per CTA (2: double buffer, 1: single)
   int64_t x_limit;     // words of x the ABI guarantees readable (checked builds)
   int64_t y_limit;
   int64_t out_words;   // words of out the run may touch (checked builds)
@@ -1025,8 +1026,9 @@ __global__ void __launch_bounds__(256, (Q > 64 ? BX_TMA_MINB_Q128 : (Q > 32 ? BX
   const int64_t B = (int64_t)Q * a.n;
   const int64_t ntiles = (a.nblocks + T - 1) / T;
   const int ow_max = (int)((31 + (int64_t)T * Q + 31) >> 5) + 2;
+  const int S = a.stages;                         // input stages (1 or 2)
   uint32_t* bufs = smem;                          // [stage][x|y][sw]
-  uint32_t* outs = smem + 4 * sw;                 // [stage][ow_max]
+  uint32_t* outs = smem + 2 * S * sw;             // [2][ow_max]
   const char* xg = reinterpret_cast<const char*>(a.x);
   const char* yg = reinterpret_cast<const char*>(a.y);
 
@@ -1057,10 +1059,10 @@ __global__ void __launch_bounds__(256, (Q > 64 ? BX_TMA_MINB_Q128 : (Q > 32 ? BX
   int64_t t = blockIdx.x;
   if (threadIdx.x == 0 && t < ntiles) issue(t, 0);
   uint32_t phase[2] = {0u, 0u};
-  int st = 0;
-  for (; t < ntiles; t += gridDim.x, st ^= 1) {
+  int st = 0, ost = 0;
+  for (; t < ntiles; t += gridDim.x, ost ^= 1) {
     const int64_t tn = t + gridDim.x;
-    if (threadIdx.x == 0 && tn < ntiles) {
+    if (S == 2 && threadIdx.x == 0 && tn < ntiles) {
       // the buffer being refilled was last read through the generic proxy
       // (before the previous iteration's __syncthreads); order those reads
       // before the async-proxy (TMA) writes
@@ -1070,7 +1072,7 @@ __global__ void __launch_bounds__(256, (Q > 64 ? BX_TMA_MINB_Q128 : (Q > 32 ? BX
     const int64_t tile0 = t * T;
     const int nb = (int)((a.nblocks - tile0) < T ? (a.nblocks - tile0) : T);
     const int64_t ostart = a.out_bit0 + tile0 * Q;
-    uint32_t* so = outs + st * ow_max;
+    uint32_t* so = outs + ost * ow_max;
     const TileWin wx = tile_window(a.x_bit0 + tile0 * B, (int64_t)nb * B);
     const TileWin wy = tile_window(a.y_bit0 + tile0 * B, (int64_t)nb * B);
     // every thread observes the phase flip itself, which makes the bulk copy's
@@ -1082,6 +1084,17 @@ __global__ void __launch_bounds__(256, (Q > 64 ? BX_TMA_MINB_Q128 : (Q > 32 ? BX
     // all of this tile's output bits are in `so` and all reads of this input
     // buffer are done (thread 0 refills it next iteration)
     __syncthreads();
+    if (S == 1) {
+      // single stage: the only input buffer is free now; its refill overlaps
+      // this tile's store and the other resident CTAs' compute (half the
+      // shared memory per CTA, twice the resident warps)
+      if (threadIdx.x == 0 && tn < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(tn, 0);
+      }
+    } else {
+      st ^= 1;
+    }
     tile_store<true>(a.out, so, ostart, ostart + (int64_t)nb * Q, a.out_words);
   }
 }

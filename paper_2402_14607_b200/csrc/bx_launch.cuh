@@ -17,6 +17,8 @@ struct LaunchCfg {
   int staged = 1;
   int threads = 256;
   int stage_words = 0;
+  int stages = 2;     // TMA kernel input stages
+  int tile0 = 0;      // TMA: the tile choose_launch planned (before the stage budget)
   size_t smem = 0;
   int64_t grid = 0;
   int family = 0;     // 0 diag, 1 holes
@@ -232,13 +234,29 @@ inline cudaError_t tma_occupancy(const void* k, int q, int threads, size_t smem,
   return cudaSuccess;
 }
 
-inline void make_tma(LaunchCfg& c, int q, int n, int64_t nblocks) {
+// Input stages of the TMA kernel: 2 = double buffer (the planned geometry,
+// what bx_launch_info reports), 1 = one buffer per CTA, i.e. twice the tile (or
+// twice the CTAs) in the same shared memory.  Unset: launch_eq picks per
+// launch from the occupancy of both (see tma_pick_stages); BX_TMA_STAGES=1/2
+// forces one, for A/B runs.
+inline int tma_stages_env() {
+  static const int v = [] {
+    const char* e = getenv("BX_TMA_STAGES");
+    const int s = e ? atoi(e) : 0;
+    return s == 1 || s == 2 ? s : 0;
+  }();
+  return v;
+}
+
+inline void make_tma(LaunchCfg& c, int q, int n, int64_t nblocks, int S = 0) {
   const size_t kTmaBudget = tma_budget(q);
   const int64_t B = (int64_t)q * n;
+  if (S == 0) S = tma_stages_env() == 1 ? 1 : 2;
   auto words = [&](int t) { return (int)((((((int64_t)t * B + 7) >> 3) + 4 + 32) + 15) / 16 * 4); };
   auto outw = [&](int t) { return (int)((31 + (int64_t)t * q + 31) >> 5) + 2; };
-  auto bytes = [&](int t) { return (size_t)(4 * (int64_t)words(t) + 2 * outw(t)) * 4; };
-  int T = c.tile;
+  auto bytes = [&](int t) { return (size_t)(2 * S * (int64_t)words(t) + 2 * outw(t)) * 4; };
+  if (!c.tma) c.tile0 = c.tile;     // the tile before any TMA budget cut
+  int T = c.tile0;
   const int Tmin = 32 >> c.tpb_log2 > 0 ? 32 >> c.tpb_log2 : 1;
   while (bytes(T) > kTmaBudget && T > Tmin) T /= 2;
   if (bytes(T) > 200 * 1024) return;  // keep the non-pipelined configuration
@@ -247,6 +265,7 @@ inline void make_tma(LaunchCfg& c, int q, int n, int64_t nblocks) {
   c.tile = T;
   c.threads = T << c.tpb_log2;
   c.stage_words = words(T);
+  c.stages = S;
   c.smem = bytes(T);
   const int64_t ntiles = (nblocks + T - 1) / T;
   const int per_sm = (int)((200 * 1024) / c.smem) > 0 ? (int)((200 * 1024) / c.smem) : 1;
@@ -264,6 +283,28 @@ cudaError_t launch_eq(const EqArgs& a, const LaunchCfg& c, cudaStream_t s) {
     int occ = 0;
     cudaError_t e = tma_occupancy(reinterpret_cast<const void*>(k), Q, c.threads, c.smem, &occ);
     if (e != cudaSuccess) return e;
+    if (c.stages == 2 && tma_stages_env() == 0) {
+      // Single-stage twin of the planned geometry: the same shared memory holds
+      // twice the tile, so a CTA has twice the threads.  It wins where the
+      // double-buffered plan leaves the SM short of warps -- the 128-register
+      // dot kernels at 32 < q <= 64 run 256 threads per SM with two stages and
+      // 512 with one (c4p -6%, q=52 n=100 -18%, q=64 n=31 -27%) -- and loses
+      // where registers already cap the resident threads or fewer than three
+      // CTAs would share an SM (nothing then overlaps a CTA's only load):
+      // q=33 n=120 +8%, q=20 n=60 +8% (profiles/r02/dp2a_sweep.txt, sweeps 17-18).
+      LaunchCfg alt = c;
+      make_tma(alt, Q, a.n, a.nblocks, 1);
+      int occ1 = 0;
+      if (alt.tma && alt.stages == 1 &&
+          tma_occupancy(reinterpret_cast<const void*>(k), Q, alt.threads, alt.smem, &occ1) == cudaSuccess &&
+          occ1 >= 3 && 2 * (int64_t)occ1 * alt.threads >= 3 * (int64_t)occ * c.threads) {
+        EqArgs a1 = a;
+        a1.tile_blocks = alt.tile;
+        a1.stage_words = alt.stage_words;
+        a1.stages = 1;
+        return launch_eq<Q>(a1, alt, s);
+      }
+    }
     const int64_t ntiles = (a.nblocks + c.tile - 1) / c.tile;
     const int64_t resident = (int64_t)sm_count() * (occ > 0 ? occ : 1);
     const int64_t grid = ntiles < resident ? ntiles : resident;
