@@ -714,6 +714,90 @@ struct Dot {
   }
 };
 
+// Dot form with the high-byte sums folded into the low-byte accumulators at
+// every step (h << 8 moves class c + 1 onto class c; bits shifted out are
+// count garbage): three accumulators per leaf like the IMAD form, for elements
+// of five to eight halves, whose 6 x K(NH) split accumulators do not fit.
+// Costs one SHF and a wider XOR per class and step; pairs only.
+__device__ __forceinline__ void dotm16(const Parts& x, const Parts& y, uint32_t (&acc)[3]) {
+  uint32_t l[3], h[3];
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    l[c] = 0u;
+    h[c] = 0u;
+#pragma unroll
+    for (int r = 0; r < 3; r++) {
+      const int s = (c + 3 - r) % 3;
+      l[c] ^= __dp2a_lo(x.p[r], y.p[s], 0u);
+      h[c] ^= __dp2a_hi(x.p[r], y.p[s], 0u);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; c++) acc[c] ^= l[c] ^ (h[(c + 1) % 3] << 8);
+}
+
+template <int M, int L0, int K>
+__device__ __forceinline__ void mkara_acc(const Parts* xo, const Parts* yo, uint32_t (&acc)[K][3]) {
+  if constexpr (M == 1) {
+    dotm16(xo[0], yo[0], acc[L0]);
+  } else {
+    constexpr int h = (M + 1) / 2;
+    mkara_acc<h, L0, K>(xo, yo, acc);
+    mkara_acc<M - h, L0 + kara_leaves(h), K>(xo + h, yo + h, acc);
+    Parts xm[h], ym[h];
+#pragma unroll
+    for (int i = 0; i < h; i++) {
+      xm[i] = (i + h < M) ? pxor(xo[i], xo[i + h]) : xo[i];
+      ym[i] = (i + h < M) ? pxor(yo[i], yo[i + h]) : yo[i];
+    }
+    mkara_acc<h, L0 + kara_leaves(h) + kara_leaves(M - h), K>(xm, ym, acc);
+  }
+}
+
+template <int Q>
+struct DotM {
+  static constexpr int EW = cdiv(Q, 32);
+  static constexpr int NH = cdiv(Q, 16);
+  static constexpr int K = kara_leaves(NH);
+  static constexpr int CW = cdiv(2 * Q - 1, 32);
+  static constexpr bool kPair = true;
+  uint32_t acc[K][3];
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int s = 0; s < K; s++) acc[s][0] = acc[s][1] = acc[s][2] = 0u;
+  }
+  __device__ __forceinline__ void add2(const uint32_t (&xa)[EW], const uint32_t (&ya)[EW],
+                                       const uint32_t (&xb)[EW], const uint32_t (&yb)[EW]) {
+    Parts px[NH], py[NH];
+    Dot<Q>::pack_x(xa, xb, px);
+    Dot<Q>::pack_y(ya, yb, py);
+    mkara_acc<NH, 0, K>(px, py, acc);
+  }
+  __device__ __forceinline__ void add(const uint32_t (&xa)[EW], const uint32_t (&ya)[EW]) {
+    uint32_t z[EW];
+#pragma unroll
+    for (int i = 0; i < EW; i++) z[i] = 0u;
+    add2(xa, ya, z, z);
+  }
+  __device__ __forceinline__ Wide<CW> unreduced() const {
+    uint32_t P[K];
+#pragma unroll
+    for (int s = 0; s < K; s++)
+      P[s] = (acc[s][0] & 0x49249249u) | (acc[s][1] & 0x92492492u) | (acc[s][2] & 0x24924924u);
+    Wide<CW> c = wzero<CW>();
+    kara_fin<NH, 0, 1u, K, CW>(P, c);
+    return c;
+  }
+};
+
+// widest element the tile kernels take in the merged form (0: off): -3..-12%
+// against the IMAD form from 16 elements per block up, +3..7% at n <= 9
+// (profiles/r02/dp2a_sweep.txt, sweep 23)
+#ifndef BX_DOTM_MAX_HALVES
+#define BX_DOTM_MAX_HALVES 8
+#endif
+
 // accumulator of the direct kernels' holes widths
 // the q = 64 direct kernel in the dot form (four elements per step): q=64 n=50
 // 0.367 -> 0.311 ms, n=64 / n=8 -9% (profiles/r02/dp2a_sweep.txt, sweep 16)
@@ -725,8 +809,10 @@ __host__ __device__ constexpr bool dot_direct_q(int q) {
 }
 // accumulator of the tile and period kernels
 template <int Q>
-using TileHoles = typename std::conditional<(BX_DP2A_TILE != 0 && cdiv(Q, 16) <= BX_DOT_TILE_MAX_HALVES),
-                                            Dot<Q>, Holes<Q>>::type;
+using TileHoles = typename std::conditional<
+    (BX_DP2A_TILE != 0 && cdiv(Q, 16) <= BX_DOT_TILE_MAX_HALVES), Dot<Q>,
+    typename std::conditional<(BX_DP2A_TILE != 0 && cdiv(Q, 16) <= BX_DOTM_MAX_HALVES), DotM<Q>,
+                              Holes<Q>>::type>::type;
 template <typename H>
 struct has_quad { static constexpr bool value = false; };
 template <int Q>

@@ -108,3 +108,30 @@ def test_packing_selectors_of_wider_elements():
         L, H, M = leaf_packed(xl, yl), leaf_packed(xh, yh), leaf_packed(xl ^ xh, yl ^ yh)
         got = L ^ ((L ^ H ^ M) << 16) ^ (H << 32)
         assert got == clmul(xa, ya) ^ clmul(xb, yb)
+
+
+def leaf_merged(pairs) -> int:
+    """DotM (csrc/bx_core.cuh: dotm16): the high-byte sums are folded into the
+    low-byte accumulators at every step, shifted by 8 -- class c + 1 lands on
+    class c, and whatever leaves the 32-bit word is count garbage."""
+    acc = [0, 0, 0]
+    for xw, yw in pairs:
+        yp = byte_perm(yw, 0, 0x3120)
+        lo, hi = [0, 0, 0], [0, 0, 0]
+        for c in range(3):
+            for r in range(3):
+                s = (c + 3 - r) % 3
+                lo[c] ^= dp2a(xw & MX[r], yp & MY[s], False)
+                hi[c] ^= dp2a(xw & MX[r], yp & MY[s], True)
+        for c in range(3):
+            acc[c] ^= lo[c] ^ ((hi[(c + 1) % 3] << 8) & 0xFFFFFFFF)
+    return (acc[0] & FIELD[0]) | (acc[1] & FIELD[1]) | (acc[2] & FIELD[2])
+
+
+def test_merged_leaf_matches_split_leaf():
+    rnd = random.Random(77)
+    cases = [[(0xFFFFFFFF, 0xFFFFFFFF)] * 64, [(0xFFFFFFFF, 0xFFFFFFFF)], [(0x80008000, 0x80808080)]]
+    cases += [[(rnd.getrandbits(32), rnd.getrandbits(32)) for _ in range(rnd.randint(1, 40))]
+              for _ in range(60)]
+    for pairs in cases:
+        assert leaf_merged(pairs) == want(pairs) & 0xFFFFFFFF
